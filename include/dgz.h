@@ -1,0 +1,224 @@
+/*
+ * dgz.h -- C ABI of libdgz: direct GPU zero-copy feature gather for GCN minibatches on B200.
+ *
+ * The operations follow arXiv 2103.03330 (PyTorch-Direct); "P:n" is /root/reference/PAPER.md
+ * line n, "S:n" is SPEC.md line n.  The boundary is described in DESIGN.md section 2.
+ *
+ * Conventions for every entry point
+ *   - Returns a dgz_status.  No exception crosses the ABI and nothing calls exit().
+ *   - DGZ_ERR_INVALID: bad argument, detected synchronously before any work is enqueued.
+ *   - DGZ_ERR_CUDA: a CUDA runtime call failed; dgz_last_error() has the CUDA error string.
+ *   - DGZ_ERR_NOMEM: host allocation / pinning failed.
+ *   - DGZ_ERR_RANGE: an index was out of range.  Device-side range faults are latched in a
+ *     device flag and reported by dgz_check_errors (the offending row is skipped, the CUDA
+ *     context is never faulted).
+ *   - DGZ_ERR_STATE: the call is not valid in the current state (e.g. wrong device).
+ *   - dgz_last_error() returns a thread-local message describing the last failure.
+ *   - "device" pointers are CUDA device (or UVA-mapped) addresses owned by the caller;
+ *     "host" pointers are ordinary process addresses.  Streams are cudaStream_t (NULL =
+ *     legacy default stream).  All enqueuing calls are asynchronous on that stream.
+ */
+#ifndef DGZ_H
+#define DGZ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGZ_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DGZ_API __attribute__((visibility("default")))
+#else
+#define DGZ_API
+#endif
+
+typedef enum {
+    DGZ_OK = 0,
+    DGZ_ERR_INVALID = 1,
+    DGZ_ERR_CUDA = 2,
+    DGZ_ERR_NOMEM = 3,
+    DGZ_ERR_RANGE = 4,
+    DGZ_ERR_STATE = 5
+} dgz_status;
+
+/* Element types of the feature table: 4 / 2 / 2 / 1 bytes.  The gather moves bytes only and
+ * never does floating-point arithmetic on them (NaN payloads are preserved; reading R17). */
+typedef enum { DGZ_F32 = 0, DGZ_F16 = 1, DGZ_BF16 = 2, DGZ_U8 = 3 } dgz_dtype;
+
+typedef struct CUstream_st* dgz_stream; /* == cudaStream_t */
+typedef struct dgz_table_s* dgz_table;  /* opaque registration handle */
+
+DGZ_API int dgz_abi_version(void);
+DGZ_API const char* dgz_last_error(void);
+/* Number of SMs of the current device (148 on B200), or -1. */
+DGZ_API int dgz_device_sm_count(void);
+
+/* ==========================================================================================
+ * Host table manager (B1).  The paper shares one host feature table between the per-GPU
+ * processes by allocating Linux shared memory first and registering it in every process
+ * (section 3.4, Listing 3).
+ * ========================================================================================== */
+#define DGZ_HOST_HUGEPAGE 1u /* madvise(MADV_HUGEPAGE) on the mapping */
+#define DGZ_HOST_POPULATE 2u /* pre-fault every page at creation */
+
+/* Map `bytes` of host memory.  shm_name == NULL: private anonymous mapping.  Otherwise a POSIX
+ * shared-memory object (/dev/shm/<name>): create != 0 creates/truncates it to `bytes`,
+ * create == 0 opens an existing object of at least `bytes` bytes.  *ptr receives a
+ * page-aligned address.  The caller releases it with dgz_host_free. */
+DGZ_API dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int create, uint32_t flags, void** ptr);
+DGZ_API dgz_status dgz_host_free(void* ptr, size_t bytes);
+DGZ_API dgz_status dgz_host_unlink(const char* shm_name);
+
+/* ==========================================================================================
+ * Table registration (step a1).  The paper's "unified tensor": cudaHostRegister page-locks
+ * the caller's host table and cudaHostGetDevicePointer maps it into the GPU address space so
+ * that kernels read it by zero-copy over PCIe, with no copy (section 3.1, tab:tensor).
+ * ========================================================================================== */
+#define DGZ_REG_PORTABLE 1u  /* cudaHostRegisterPortable: valid on every device of this process */
+#define DGZ_REG_READONLY 2u  /* cudaHostRegisterReadOnly when the device supports it */
+#define DGZ_REG_NO_PIN 4u    /* memory is already page-locked (e.g. cudaHostAlloc): map only */
+
+/* host_ptr: row 0 of a row-major, unpadded rows x dim table of `dtype` elements in host
+ * memory (any alignment; unaligned bases are a first-class case, S:37 base_offset).  The caller
+ * owns the memory and must keep it alive and unmodified-in-size until dgz_unregister_table.
+ * Registers on the CURRENT device.  rows >= 1, dim >= 1.  Pages shared with another
+ * registration are accepted (already-registered pages are mapped, not re-pinned). */
+DGZ_API dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int64_t dim, dgz_dtype dtype,
+                              uint32_t flags, dgz_table* out);
+DGZ_API dgz_status dgz_unregister_table(dgz_table t);
+
+typedef struct {
+    const void* dev_ptr;     /* device-visible address of row 0 */
+    int64_t rows, dim, row_bytes;
+    int32_t elem_bytes;
+    int32_t device;          /* device the registration was made on */
+    int32_t base_mod128;     /* (address of row 0) mod 128: the misalignment of the table */
+    int32_t flags;
+    int64_t pinned_bytes;    /* page-rounded span that was registered by this handle */
+    int64_t gpu_mem_delta;   /* device memory consumed by the mapping (~bytes/512) */
+    double register_seconds; /* wall time of cudaHostRegister */
+} dgz_table_info;
+DGZ_API dgz_status dgz_table_get_info(dgz_table t, dgz_table_info* info);
+
+/* ==========================================================================================
+ * Sparse feature gather (step a4, the hot path).
+ *   out[r*R + b] = table[idx[r]*R + b]   for 0 <= r < n, 0 <= b < R = dim * elem_bytes
+ * (Listing 2, last line "dst[dstOffset] = src[srcOffset]"; the circular shift and
+ * the segment plan only change which thread copies which byte).  Each row is
+ * fetched as its 128 B-aligned line segments (one PCIe read per line the row touches, the
+ * per-row minimum).  Byte-exact; duplicates allowed; n == 0 is a no-op.
+ * idx_dev: device int64 (or int32 for *_i32) [n].  out_dev: device [n x R] bytes, aligned to
+ * the element size, not aliasing the table.  IDs < 0 or >= rows: the row is skipped (its
+ * output bytes are left unchanged) and the table's RANGE flag is latched (dgz_check_errors).
+ * ========================================================================================== */
+DGZ_API dgz_status dgz_gather(dgz_table t, const int64_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream);
+DGZ_API dgz_status dgz_gather_i32(dgz_table t, const int32_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream);
+
+typedef enum {
+    DGZ_GATHER_AUTO = 0,    /* = SEGMENT */
+    DGZ_GATHER_SEGMENT = 1, /* 128 B-segment plan, 16 B vector loads, warp-cooperative rows */
+    DGZ_GATHER_NAIVE = 2,   /* ablation K1n: one element per thread, no alignment */
+    DGZ_GATHER_SHIFT = 3,   /* ablation: Listing 2 circular shift, one element per thread */
+    DGZ_GATHER_BULK = 4     /* cp.async.bulk (TMA engine) row copies via shared memory */
+} dgz_gather_variant;
+
+typedef struct {
+    int32_t variant;       /* dgz_gather_variant */
+    int32_t sm_count;      /* 0 = every SM; k > 0 bounds the persistent grid to k CTAs, one per
+                              SM (the B200 analogue of the paper's MPS X%, step a6) */
+    int32_t warps_per_cta; /* 0 = default */
+    int32_t ctas_per_sm;   /* 0 = default (1 when sm_count > 0) */
+} dgz_gather_cfg;
+
+/* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
+ * gathers min(*n_dev, n) rows (n is the capacity), so a gather can follow the sampler on the
+ * same stream without a host round trip.  cfg may be NULL (defaults). */
+DGZ_API dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n, const int64_t* n_dev,
+                         void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream);
+
+/* Synchronises `stream`, reads and clears the table's device RANGE flag for the current
+ * device: DGZ_ERR_RANGE if any gather since the last check met an out-of-range ID. */
+DGZ_API dgz_status dgz_check_errors(dgz_table t, dgz_stream stream);
+
+/* ==========================================================================================
+ * Layered uniform neighbour sampling on the GPU (steps a2-a3; section 2.2).
+ *   F_0 = seeds (duplicates dropped, first occurrence kept)
+ *   hop k = 0..L-1, f = fanouts[k]: every u in F_k selects min(f, deg u) distinct CSR slots
+ *     uniformly without replacement (Floyd's algorithm, r(t) = word 0 of Philox4x32-10 with
+ *     counter (t, k, lo32 u, hi32 u) and key (lo32 rng_seed, hi32 rng_seed); reading R11);
+ *     new = sorted unique(selected IDs) \ F_k;  F_{k+1} = F_k ++ new  (readings R9-R10)
+ *   ids = F_L, the gather list (seeds included).
+ * The result depends only on (csr, seeds, fanouts, rng_seed): not on grid, device or timing.
+ * ========================================================================================== */
+typedef struct {
+    int64_t n_nodes;
+    const int64_t* offsets; /* device [n_nodes + 1], offsets[0] = 0, non-decreasing */
+    const void* cols;       /* device [offsets[n_nodes]] int32 or int64 node IDs < n_nodes (NULL if no edges) */
+    int32_t cols_is64;
+    int32_t reserved;
+} dgz_csr;
+
+#define DGZ_MAX_FANOUT 64
+#define DGZ_MAX_LAYERS 8
+
+typedef struct {
+    int64_t* ids;          /* device [ids_cap] >= bounds[L]: frontier-prefix unique IDs */
+    int64_t ids_cap;
+    int64_t* sizes_dev;    /* device [L + 1]: |F_0| .. |F_L| (required) */
+    int64_t* sizes_host;   /* optional pinned host [L + 1]: async copy of sizes_dev */
+    int64_t* nbr;          /* optional device: hop k block at sum_{i<k} bounds[i]*fanouts[i],
+                              bounds[k] x fanouts[k] row-major sampled IDs, unused slots -1 */
+    int32_t* nbr_local;    /* optional device, layout of nbr: position of the ID in ids */
+    int32_t* cnt;          /* optional device: hop k block at sum_{i<k} bounds[i]: counts */
+    int64_t blocks_cap;    /* elements available in nbr / nbr_local */
+    int64_t cnt_cap;       /* elements available in cnt */
+    void* workspace;       /* device scratch of dgz_sample_workspace_bytes() bytes; not */
+    size_t workspace_bytes;/* shared between calls that may run concurrently */
+} dgz_sample_out;
+
+/* bounds[k] = min(n_nodes, n_seeds * prod_{i<k}(1 + fanouts[i])) for k = 0..L; also the
+ * element counts the optional block outputs need.  Any pointer may be NULL. */
+DGZ_API dgz_status dgz_sample_bounds(int64_t n_nodes, int64_t n_seeds, const int32_t* fanouts, int n_layers,
+                             int64_t* bounds, int64_t* blocks_elems, int64_t* cnt_elems);
+DGZ_API dgz_status dgz_sample_workspace_bytes(int64_t n_nodes, int64_t max_seeds, size_t* bytes);
+/* seeds_dev: device int64 [n_seeds], each in [0, n_nodes) (else DGZ_ERR_RANGE is latched in
+ * the workspace and reported by dgz_sample_check; offending seeds are dropped).
+ * fanouts: HOST int32 [n_layers], 0 <= f <= DGZ_MAX_FANOUT, n_layers <= DGZ_MAX_LAYERS. */
+DGZ_API dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seeds_dev, int64_t n_seeds,
+                              const int32_t* fanouts, int n_layers, uint64_t rng_seed,
+                              const dgz_sample_out* out, dgz_stream stream);
+/* Synchronises `stream`; DGZ_ERR_RANGE if a seed was out of range in the last call. */
+DGZ_API dgz_status dgz_sample_check(const dgz_sample_out* out, dgz_stream stream);
+
+/* ==========================================================================================
+ * Stand-in GraphSAGE mean aggregation (consumer, step a7; P:554-555 fig:singlegpu): for dst
+ * node i < *n_dst_dev (bounded by n_dst_max):
+ *   y[i, :] = (x[i, :] + sum_{c < cnt[i]} x[nbr_local[i*fanout + c], :]) / (1 + cnt[i])
+ * over fp32 rows x [*, dim].  `repeat` re-runs the aggregation to scale the consumer's work
+ * (T_c ~ T_g for the overlap measurement).  Not on the parity path.
+ * ========================================================================================== */
+DGZ_API dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int32_t* nbr_local, const int32_t* cnt,
+                              int32_t fanout, const int64_t* n_dst_dev, int64_t n_dst_max, float* y,
+                              int32_t repeat, int32_t sm_count, dgz_stream stream);
+
+/* ==========================================================================================
+ * PCIe probes (the zero-copy ceiling and the round-trip time).
+ * ========================================================================================== */
+/* Streaming zero-copy read of `bytes` (multiple of 16) from a mapped host pointer with 16 B
+ * loads, `warps` warps on each of `sm_count` SMs, each warp keeping `unroll` loads in flight.
+ * A checksum is written to *sink_dev so the loads cannot be elided. */
+DGZ_API dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32_t sm_count, int32_t warps,
+                            int32_t unroll, uint64_t* sink_dev, dgz_stream stream);
+/* Dependent-load chain of `steps` hops through a mapped host array of int64 "next" offsets;
+ * writes cycles_dev[0] = total cycles, cycles_dev[1] = final offset (one thread;
+ * RTT = cycles / steps / SM clock).  cycles_dev: device uint64 [2]. */
+DGZ_API dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGZ_H */

@@ -1,0 +1,9 @@
+"""paper_2103_03330_b200 -- direct GPU zero-copy feature gather for GCN minibatches (B200).
+
+B200-native rebuild of the hot path of arXiv 2103.03330 (PyTorch-Direct): layered uniform
+sampling on the GPU and the sparse feature gather that reads rows of a pinned, mapped host
+table over PCIe with zero-copy loads and writes them densely into HBM.  The compute is in
+``libdgz.so`` (CUDA, sm_100a; C ABI in ``include/dgz.h``); ``dgz`` is its thin binding and
+``pipeline`` the per-GPU minibatch fetcher (ping-pong buffers, side stream).
+"""
+from . import dgz  # noqa: F401  (raises ImportError if libdgz.so is missing: no fallback)

@@ -1,0 +1,249 @@
+// libdgz: error state, host table manager (B1) and table registration (step a1).
+//   Registration = the paper's "unified tensor" (section 3.1): cudaHostRegister
+//   page-locks the caller's table, cudaHostGetDevicePointer maps it for zero-copy access.
+//   Shared host memory across per-GPU processes = P:616-627 section 3.4 (Listing 3).
+#include <errno.h>
+#include <fcntl.h>
+#include <stdarg.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <mutex>
+
+#include "internal.h"
+
+namespace dgz {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+dgz_status cuda_fail(cudaError_t e, const char* what) {
+    set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    return DGZ_ERR_CUDA;
+}
+
+int sm_count_of_current_device() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return n;
+}
+
+static double now_s() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
+}  // namespace dgz
+
+using namespace dgz;
+
+extern "C" int dgz_abi_version(void) { return DGZ_ABI_VERSION; }
+extern "C" const char* dgz_last_error(void) { return g_err; }
+extern "C" int dgz_device_sm_count(void) { return sm_count_of_current_device(); }
+
+// ---------------------------------------------------------------------------------------------
+// Host table manager
+// ---------------------------------------------------------------------------------------------
+extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int create, uint32_t flags, void** ptr) {
+    DGZ_REQUIRE(ptr && bytes > 0, "dgz_host_alloc: null ptr or zero size");
+    *ptr = nullptr;
+    void* p = MAP_FAILED;
+    if (!shm_name) {
+        p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    } else {
+        DGZ_REQUIRE(shm_name[0] == '/', "dgz_host_alloc: shm name must start with '/'");
+        int fd = shm_open(shm_name, O_RDWR | (create ? O_CREAT : 0), 0600);
+        if (fd < 0) { set_error("shm_open(%s): %s", shm_name, strerror(errno)); return DGZ_ERR_NOMEM; }
+        if (create) {
+            if (ftruncate(fd, (off_t)bytes) != 0) {
+                set_error("ftruncate(%s, %zu): %s", shm_name, bytes, strerror(errno));
+                close(fd);
+                return DGZ_ERR_NOMEM;
+            }
+        } else {
+            struct stat st;
+            if (fstat(fd, &st) != 0 || (size_t)st.st_size < bytes) {
+                set_error("shm object %s smaller than %zu bytes", shm_name, bytes);
+                close(fd);
+                return DGZ_ERR_INVALID;
+            }
+        }
+        p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+    }
+    if (p == MAP_FAILED) { set_error("mmap(%zu): %s", bytes, strerror(errno)); return DGZ_ERR_NOMEM; }
+    if (flags & DGZ_HOST_HUGEPAGE) madvise(p, bytes, MADV_HUGEPAGE);
+    if (flags & DGZ_HOST_POPULATE) {
+        volatile uint8_t* b = (volatile uint8_t*)p;
+        long pg = sysconf(_SC_PAGESIZE);
+        for (size_t off = 0; off < bytes; off += (size_t)pg) b[off] = b[off];
+    }
+    *ptr = p;
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_host_free(void* ptr, size_t bytes) {
+    DGZ_REQUIRE(ptr && bytes > 0, "dgz_host_free: null ptr or zero size");
+    if (munmap(ptr, bytes) != 0) { set_error("munmap: %s", strerror(errno)); return DGZ_ERR_INVALID; }
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_host_unlink(const char* shm_name) {
+    DGZ_REQUIRE(shm_name, "dgz_host_unlink: null name");
+    if (shm_unlink(shm_name) != 0 && errno != ENOENT) {
+        set_error("shm_unlink(%s): %s", shm_name, strerror(errno));
+        return DGZ_ERR_INVALID;
+    }
+    return DGZ_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Registration
+// ---------------------------------------------------------------------------------------------
+static int elem_bytes_of(dgz_dtype d) {
+    switch (d) {
+        case DGZ_F32: return 4;
+        case DGZ_F16: return 2;
+        case DGZ_BF16: return 2;
+        case DGZ_U8: return 1;
+    }
+    return 0;
+}
+
+extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int64_t dim, dgz_dtype dtype,
+                                         uint32_t flags, dgz_table* out) {
+    DGZ_REQUIRE(out, "dgz_register_table: null out");
+    *out = nullptr;
+    DGZ_REQUIRE(host_ptr, "dgz_register_table: null host_ptr");
+    DGZ_REQUIRE(rows >= 1 && dim >= 1, "dgz_register_table: rows=%lld dim=%lld", (long long)rows, (long long)dim);
+    int eb = elem_bytes_of(dtype);
+    DGZ_REQUIRE(eb > 0, "dgz_register_table: unknown dtype %d", (int)dtype);
+    DGZ_REQUIRE(dim <= (int64_t(1) << 40) / eb && rows <= (int64_t(1) << 62) / (dim * eb),
+                "dgz_register_table: table too large");
+    DGZ_REQUIRE(((uintptr_t)host_ptr % eb) == 0, "dgz_register_table: host_ptr not aligned to the element size");
+
+    dgz_table t = new (std::nothrow) dgz_table_s();
+    if (!t) { set_error("out of memory"); return DGZ_ERR_NOMEM; }
+    t->host = (const uint8_t*)host_ptr;
+    t->rows = rows;
+    t->dim = dim;
+    t->elem_bytes = eb;
+    t->row_bytes = dim * eb;
+    t->flags = flags;
+    cudaError_t e = cudaGetDevice(&t->device);
+    if (e != cudaSuccess) { delete t; return cuda_fail(e, "cudaGetDevice"); }
+
+    const size_t bytes = (size_t)rows * (size_t)t->row_bytes;
+    const uintptr_t pg = (uintptr_t)sysconf(_SC_PAGESIZE);
+    uintptr_t lo = (uintptr_t)host_ptr & ~(pg - 1);
+    uintptr_t hi = ((uintptr_t)host_ptr + bytes + pg - 1) & ~(pg - 1);
+
+    size_t free0 = 0, free1 = 0, total = 0;
+    cudaMemGetInfo(&free0, &total);
+    double t0 = now_s();
+    if (!(flags & DGZ_REG_NO_PIN)) {
+        unsigned int rf = cudaHostRegisterMapped;
+        if (flags & DGZ_REG_PORTABLE) rf |= cudaHostRegisterPortable;
+        if (flags & DGZ_REG_READONLY) {
+            int ro = 0;
+            cudaDeviceGetAttribute(&ro, cudaDevAttrHostRegisterReadOnlySupported, t->device);
+            if (ro) rf |= cudaHostRegisterReadOnly;
+        }
+        e = cudaHostRegister((void*)lo, hi - lo, rf);
+        if (e == cudaErrorHostMemoryAlreadyRegistered) {
+            cudaGetLastError();  // pages already registered by someone else: map only
+        } else if (e != cudaSuccess) {
+            delete t;
+            return cuda_fail(e, "cudaHostRegister");
+        } else {
+            t->reg_base = (void*)lo;
+            t->reg_bytes = hi - lo;
+        }
+    }
+    t->register_seconds = now_s() - t0;
+    void* dptr = nullptr;
+    e = cudaHostGetDevicePointer(&dptr, (void*)host_ptr, 0);
+    if (e != cudaSuccess) {
+        if (t->reg_base) cudaHostUnregister(t->reg_base);
+        delete t;
+        return cuda_fail(e, "cudaHostGetDevicePointer");
+    }
+    cudaMemGetInfo(&free1, &total);
+    t->gpu_mem_delta = (int64_t)free0 - (int64_t)free1;
+    t->dev = (const uint8_t*)dptr;
+    *out = t;
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_unregister_table(dgz_table t) {
+    DGZ_REQUIRE(t, "dgz_unregister_table: null table");
+    dgz_status st = DGZ_OK;
+    for (int d = 0; d < 64; d++) {
+        if (t->err_flag[d]) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            cudaFree(t->err_flag[d]);
+            cudaSetDevice(cur);
+        }
+    }
+    if (t->reg_base) {
+        cudaError_t e = cudaHostUnregister(t->reg_base);
+        if (e != cudaSuccess) st = cuda_fail(e, "cudaHostUnregister");
+    }
+    delete t;
+    return st;
+}
+
+extern "C" dgz_status dgz_table_get_info(dgz_table t, dgz_table_info* info) {
+    DGZ_REQUIRE(t && info, "dgz_table_get_info: null argument");
+    info->dev_ptr = t->dev;
+    info->rows = t->rows;
+    info->dim = t->dim;
+    info->row_bytes = t->row_bytes;
+    info->elem_bytes = t->elem_bytes;
+    info->device = t->device;
+    info->base_mod128 = (int32_t)((uintptr_t)t->dev & 127);
+    info->flags = (int32_t)t->flags;
+    info->pinned_bytes = (int64_t)t->reg_bytes;
+    info->gpu_mem_delta = t->gpu_mem_delta;
+    info->register_seconds = t->register_seconds;
+    return DGZ_OK;
+}
+
+static std::mutex g_flag_mu;
+
+int* dgz_table_flag(dgz_table t) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(g_flag_mu);
+    if (!t->err_flag[dev]) {
+        int* f = nullptr;
+        if (cudaMalloc(&f, sizeof(int)) != cudaSuccess) return nullptr;
+        if (cudaMemset(f, 0, sizeof(int)) != cudaSuccess) { cudaFree(f); return nullptr; }
+        t->err_flag[dev] = f;
+    }
+    return t->err_flag[dev];
+}
+
+extern "C" dgz_status dgz_check_errors(dgz_table t, dgz_stream stream) {
+    DGZ_REQUIRE(t, "dgz_check_errors: null table");
+    int* f = dgz_table_flag(t);
+    if (!f) { set_error("dgz_check_errors: cannot allocate the device flag"); return DGZ_ERR_CUDA; }
+    int h = 0;
+    DGZ_CUDA(cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    DGZ_CUDA(cudaMemsetAsync(f, 0, sizeof(int), (cudaStream_t)stream));
+    DGZ_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (h) { set_error("gather met an index outside [0, rows)"); return DGZ_ERR_RANGE; }
+    return DGZ_OK;
+}

@@ -1,0 +1,306 @@
+// Sparse feature gather over PCIe zero-copy (step a4, the hot path).
+//
+//   out[r*R + b] = table[idx[r]*R + b]     (Listing 2; closed form)
+//
+// SEGMENT kernel (the product).  The paper's circular shift (fig:auto_alignment)
+// exists so that a warp's loads start on 128 B line boundaries and every PCIe read request
+// carries as many useful bytes as possible.  On sm_100a we get the same goal directly, per
+// row: a row that starts at byte a and has R bytes touches L = ceil(((a mod 128) + R) / 128)
+// lines, and the kernel issues exactly one warp-cooperative 128 B-aligned segment load per
+// line (8 lanes x 16 B, LDG.E.128), i.e. the per-row minimum number of PCIe reads (SURVEY
+// 8(a) a4').  A warp owns 32 rows at a time; lane i loads row i's ID, computes its line count,
+// and a warp inclusive scan turns the 32 rows into a flat list of line tasks; each warp load
+// instruction serves 4 line tasks (4 groups of 8 lanes), U instructions are issued back to
+// back before any store so that 4*U lines per warp are in flight over PCIe.  Loads are always
+// 16 B and line aligned (whatever the row alignment: sectors are fetched whole anyway);
+// stores go to HBM in the widest piece SW in {16,8,4,2,1} that divides R and both base
+// addresses, so no byte outside the row is ever written and no shared-memory realignment is
+// needed.  HBM stores of a warp instruction are contiguous per line group (coalesced).
+//
+// NAIVE / SHIFT kernels: the paper's Listing 2 without / with the circular shift stage, one
+// element per thread (ablations for the fig:alignment_measurement analogue).  The shift
+// aligns to 128 BYTES (W = 128 / sizeof(T) elements; reading R3) with 64-bit offsets (R4).
+#include "internal.h"
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_zc_v4(uint64_t p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+template <int SW>
+__device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo, int hi) {
+    // store bytes [lo, hi) of the 16-byte chunk v (lo, hi multiples of SW) at d + byte
+    if constexpr (SW == 16) {
+        *reinterpret_cast<uint4*>(d) = v;
+    } else if constexpr (SW == 8) {
+        const uint2 p0 = make_uint2(v.x, v.y), p1 = make_uint2(v.z, v.w);
+        if (lo <= 0 && hi >= 8) *reinterpret_cast<uint2*>(d) = p0;
+        if (lo <= 8 && hi >= 16) *reinterpret_cast<uint2*>(d + 8) = p1;
+    } else if constexpr (SW == 4) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+            if (p * 4 >= lo && p * 4 < hi) *reinterpret_cast<uint32_t*>(d + 4 * p) = w[p];
+    } else if constexpr (SW == 2) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+            if (p * 2 >= lo && p * 2 < hi)
+                *reinterpret_cast<uint16_t*>(d + 2 * p) = (uint16_t)(w[p >> 1] >> (16 * (p & 1)));
+    } else {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int p = 0; p < 16; ++p)
+            if (p >= lo && p < hi) *reinterpret_cast<uint8_t*>(d + p) = (uint8_t)(w[p >> 2] >> (8 * (p & 3)));
+    }
+}
+
+template <int SW, int U, typename IdxT>
+__global__ void __launch_bounds__(1024, 1)
+gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
+                      int64_t n_cap, const int64_t* __restrict__ n_dev, uint8_t* __restrict__ dst,
+                      int* __restrict__ err) {
+    int64_t n = n_cap;
+    if (n_dev) {
+        const int64_t m = *n_dev;
+        n = m < n_cap ? m : n_cap;
+    }
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 3;
+    const int sub = lane & 7;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t base = reinterpret_cast<uint64_t>(src);
+    const uint64_t dbase = reinterpret_cast<uint64_t>(dst);
+
+    int64_t b0 = warp * 32;
+    // software-pipelined ID load: the next batch's ID is fetched before this batch's PCIe loads
+    int64_t id_next = -1;
+    if (b0 + lane < n) id_next = (int64_t)idx[b0 + lane];
+
+    for (; b0 < n; b0 += nwarps * 32) {
+        const int64_t r = b0 + lane;
+        int64_t id = id_next;
+        {
+            const int64_t rn = r + nwarps * 32;
+            id_next = rn < n ? (int64_t)idx[rn] : -1;
+        }
+        if (r < n && (id < 0 || id >= rows)) {
+            atomicOr(err, 1);
+            id = -1;
+        }
+        if (r >= n) id = -1;
+        const uint64_t a = base + (uint64_t)(id < 0 ? 0 : id) * (uint64_t)R;
+        const uint64_t l0 = a & ~uint64_t(127);
+        const int nl = id < 0 ? 0 : (int)((a + (uint64_t)R - l0 + 127) >> 7);
+        int incl = nl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int excl = incl - nl;
+        const int T = __shfl_sync(0xffffffffu, incl, 31);
+
+        for (int t0 = 0; t0 < T; t0 += 4 * U) {
+            uint4 v[U];
+            int pk[U];  // (offset of the chunk in its row + 128) << 5 | row lane, or -1 if idle
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int tb = t0 + 4 * u;
+                const unsigned m0 = __ballot_sync(0xffffffffu, incl <= tb);
+                const unsigned m1 = __ballot_sync(0xffffffffu, incl <= tb + 1);
+                const unsigned m2 = __ballot_sync(0xffffffffu, incl <= tb + 2);
+                const unsigned m3 = __ballot_sync(0xffffffffu, incl <= tb + 3);
+                const unsigned m = g == 0 ? m0 : (g == 1 ? m1 : (g == 2 ? m2 : m3));
+                const int t = tb + g;
+                const int rho = __popc(m);  // first lane whose inclusive count exceeds t
+                const int sl = rho < 32 ? rho : 31;
+                const uint64_t ar = __shfl_sync(0xffffffffu, a, sl);
+                const int er = __shfl_sync(0xffffffffu, excl, sl);
+                // chunk = 16 B piece `sub` of line (t - er) of the row's 128 B-aligned segment list
+                const int q = (int)(ar & 127u);  // row start offset within its first line
+                const int cq = (t - er) * 128 + sub * 16 - q;  // chunk start relative to the row start
+                const bool act = (t < T) && (cq + 16 > 0) && (cq < (int)R);
+                pk[u] = act ? (((cq + 128) << 5) | sl) : -1;
+                if (act) v[u] = ld_zc_v4(ar + (uint64_t)(int64_t)cq);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (pk[u] >= 0) {
+                    const int cq = (pk[u] >> 5) - 128;
+                    const int sl = pk[u] & 31;
+                    const uint64_t d = dbase + (uint64_t)(b0 + sl) * (uint64_t)R + (uint64_t)(int64_t)cq;
+                    store_pieces<SW>(d, v[u], cq < 0 ? -cq : 0, (int)R - cq > 16 ? 16 : (int)R - cq);
+                }
+            }
+        }
+    }
+}
+
+// Listing 2, one element per thread; SHIFT adds the circular-shift stage.
+template <typename T, bool SHIFT, typename IdxT>
+__global__ void __launch_bounds__(512)
+gather_elem_kernel(const T* __restrict__ src, int64_t rows, int64_t F, const IdxT* __restrict__ idx, int64_t n_cap,
+                   const int64_t* __restrict__ n_dev, T* __restrict__ dst, int* __restrict__ err) {
+    int64_t n = n_cap;
+    if (n_dev) {
+        const int64_t m = *n_dev;
+        n = m < n_cap ? m : n_cap;
+    }
+    constexpr int64_t W = 128 / sizeof(T);  // 128 bytes in elements (reading R3)
+    const int64_t num = n * F;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < num; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t dst_idx = i / F;
+        const int64_t offset = i % F;  // reading R1 (P:406-407 garbled)
+        const int64_t id = (int64_t)idx[dst_idx];
+        if (id < 0 || id >= rows) {
+            if (offset == 0) atomicOr(err, 1);
+            continue;
+        }
+        const int64_t dst_start = dst_idx * F;
+        const int64_t src_start = id * F;
+        int64_t dst_off = offset + dst_start;
+        int64_t src_off = offset + src_start;
+        if (SHIFT && F > W && (F % W)) {
+            int64_t diff = (dst_start - src_start) % W;
+            diff = diff < 0 ? diff + W : diff;
+            dst_off += diff;
+            src_off += diff;
+            if (src_off < src_start) {
+                dst_off += F;
+                src_off += F;
+            } else if (src_off >= src_start + F) {
+                dst_off -= F;
+                src_off -= F;
+            }
+        }
+        dst[dst_off] = src[src_off];
+    }
+}
+
+template <int SW, typename IdxT>
+cudaError_t launch_segment(const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, uint8_t* out, int* err,
+                           int blocks, int threads, cudaStream_t s) {
+    gather_segment_kernel<SW, 8, IdxT><<<blocks, threads, 0, s>>>(t->dev, t->rows, t->row_bytes, idx, n, n_dev, out, err);
+    return cudaGetLastError();
+}
+
+template <typename IdxT>
+cudaError_t launch_segment_sw(int sw, const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, uint8_t* out,
+                              int* err, int blocks, int threads, cudaStream_t s) {
+    switch (sw) {
+        case 16: return launch_segment<16>(t, idx, n, n_dev, out, err, blocks, threads, s);
+        case 8: return launch_segment<8>(t, idx, n, n_dev, out, err, blocks, threads, s);
+        case 4: return launch_segment<4>(t, idx, n, n_dev, out, err, blocks, threads, s);
+        case 2: return launch_segment<2>(t, idx, n, n_dev, out, err, blocks, threads, s);
+        default: return launch_segment<1>(t, idx, n, n_dev, out, err, blocks, threads, s);
+    }
+}
+
+template <bool SHIFT, typename IdxT>
+cudaError_t launch_elem(const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, void* out, int* err, int blocks,
+                        cudaStream_t s) {
+    switch (t->elem_bytes) {
+        case 4:
+            gather_elem_kernel<uint32_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint32_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
+                                                                           (uint32_t*)out, err);
+            break;
+        case 2:
+            gather_elem_kernel<uint16_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint16_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
+                                                                           (uint16_t*)out, err);
+            break;
+        default:
+            gather_elem_kernel<uint8_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint8_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
+                                                                          (uint8_t*)out, err);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+using namespace dgz;
+
+dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, int64_t n, const int64_t* n_dev, void* out,
+                           int* err, int sms, int warps, int ctas_per_sm, cudaStream_t s);
+
+dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n, const int64_t* n_dev, void* out,
+                           const dgz_gather_cfg* cfg, cudaStream_t s) {
+    DGZ_REQUIRE(t, "dgz_gather: null table");
+    DGZ_REQUIRE(n >= 0, "dgz_gather: n < 0");
+    if (n == 0) return DGZ_OK;
+    DGZ_REQUIRE(idx && out, "dgz_gather: null idx or out");
+    DGZ_REQUIRE(((uintptr_t)out % (uintptr_t)t->elem_bytes) == 0, "dgz_gather: out not aligned to the element size");
+    {
+        const uint8_t* o = (const uint8_t*)out;
+        const uint8_t* tb = t->host;
+        const uint8_t* te = t->host + t->rows * t->row_bytes;
+        DGZ_REQUIRE(o + n * t->row_bytes <= tb || o >= te, "dgz_gather: out aliases the table");
+    }
+    int dev = 0;
+    DGZ_CUDA(cudaGetDevice(&dev));
+    if (dev != t->device && !(t->flags & DGZ_REG_PORTABLE)) {
+        set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
+        return DGZ_ERR_STATE;
+    }
+    int* err = dgz_table_flag(t);
+    if (!err) { set_error("dgz_gather: cannot allocate the device flag"); return DGZ_ERR_CUDA; }
+    const int nsm = sm_count_of_current_device();
+    int variant = cfg ? cfg->variant : DGZ_GATHER_AUTO;
+    int k = (cfg && cfg->sm_count > 0) ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : nsm;
+    const bool bounded = cfg && cfg->sm_count > 0;
+    int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta : (bounded ? 32 : 16);
+    if (warps > 32) warps = 32;
+    int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : 1;
+    if (warps * cps > 64) cps = 64 / warps > 0 ? 64 / warps : 1;
+    if (variant == DGZ_GATHER_AUTO) variant = DGZ_GATHER_SEGMENT;
+
+    cudaError_t e = cudaSuccess;
+    if (variant == DGZ_GATHER_SEGMENT) {
+        DGZ_REQUIRE(t->row_bytes < (int64_t(1) << 25), "dgz_gather: rows of 32 MiB or more are not supported");
+        int64_t batches = (n + 31) / 32;
+        int64_t blocks = (int64_t)k * cps;
+        int64_t need = (batches + warps - 1) / warps;
+        if (blocks > need) blocks = need;
+        const uint64_t x = (uint64_t)t->row_bytes | ((uint64_t)(uintptr_t)t->dev & 15u) | ((uint64_t)(uintptr_t)out & 15u) | 16u;
+        const int sw = (int)(x & (~x + 1));
+        if (idx_is64)
+            e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, s);
+        else
+            e = launch_segment_sw<int32_t>(sw, t, (const int32_t*)idx, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, s);
+    } else if (variant == DGZ_GATHER_NAIVE || variant == DGZ_GATHER_SHIFT) {
+        int64_t blocks = (int64_t)k * 4;
+        const bool sh = variant == DGZ_GATHER_SHIFT;
+        if (idx_is64)
+            e = sh ? launch_elem<true>(t, (const int64_t*)idx, n, n_dev, out, err, (int)blocks, s)
+                   : launch_elem<false>(t, (const int64_t*)idx, n, n_dev, out, err, (int)blocks, s);
+        else
+            e = sh ? launch_elem<true>(t, (const int32_t*)idx, n, n_dev, out, err, (int)blocks, s)
+                   : launch_elem<false>(t, (const int32_t*)idx, n, n_dev, out, err, (int)blocks, s);
+    } else if (variant == DGZ_GATHER_BULK) {
+        return dgz_gather_bulk(t, idx, idx_is64, n, n_dev, out, err, k, warps, cps, s);
+    } else {
+        set_error("dgz_gather: unknown variant %d", variant);
+        return DGZ_ERR_INVALID;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "gather kernel launch");
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_gather(dgz_table t, const int64_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
+    return dgz_gather_impl(t, idx_dev, 1, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" dgz_status dgz_gather_i32(dgz_table t, const int32_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
+    return dgz_gather_impl(t, idx_dev, 0, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n, const int64_t* n_dev, void* out_dev,
+                                    const dgz_gather_cfg* cfg, dgz_stream stream) {
+    return dgz_gather_impl(t, idx_dev, 1, n, n_dev, out_dev, cfg, (cudaStream_t)stream);
+}

@@ -1,0 +1,53 @@
+// Internal helpers shared by the libdgz translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "dgz.h"
+
+namespace dgz {
+
+void set_error(const char* fmt, ...);
+dgz_status cuda_fail(cudaError_t e, const char* what);
+
+#define DGZ_CUDA(call)                                                 \
+    do {                                                               \
+        cudaError_t _e = (call);                                       \
+        if (_e != cudaSuccess) return ::dgz::cuda_fail(_e, #call);     \
+    } while (0)
+
+#define DGZ_REQUIRE(cond, ...)                                         \
+    do {                                                               \
+        if (!(cond)) { ::dgz::set_error(__VA_ARGS__); return DGZ_ERR_INVALID; } \
+    } while (0)
+
+inline dgz_status launch_check(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    return DGZ_OK;
+}
+
+int sm_count_of_current_device();
+
+}  // namespace dgz
+
+struct dgz_table_s {
+    const uint8_t* host;      // caller's pointer to row 0
+    const uint8_t* dev;       // device-visible pointer to row 0
+    int64_t rows, dim, row_bytes;
+    int32_t elem_bytes;
+    int32_t device;
+    uint32_t flags;
+    void* reg_base;           // page-aligned base that this handle registered (nullptr if none)
+    size_t reg_bytes;
+    int64_t gpu_mem_delta;
+    double register_seconds;
+    int* err_flag[64];        // per-device RANGE flag (device memory), lazily allocated
+};
+
+// gather.cu
+dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n, const int64_t* n_dev,
+                           void* out, const dgz_gather_cfg* cfg, cudaStream_t stream);
+int* dgz_table_flag(dgz_table t);  // flag for the current device (allocates on first use)

@@ -1,0 +1,73 @@
+// PCIe zero-copy probes: the streaming-read ceiling of GPU-initiated loads
+// over the link, and the round-trip time of one dependent load (the paper's Little's-law
+// inputs).
+#include "internal.h"
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_zc(uint64_t p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+template <int U>
+__global__ void __launch_bounds__(1024, 1) stream_kernel(const uint8_t* __restrict__ src, int64_t chunks, uint64_t* sink) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    uint32_t acc = 0;
+    for (int64_t c0 = w * 32 * U; c0 < chunks; c0 += nw * 32 * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = c0 + u * 32 + lane;
+            if (c < chunks) v[u] = ld_zc((uint64_t)src + (uint64_t)c * 16);
+            else v[u] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    if (acc == 0x9E3779B9u) atomicAdd((unsigned long long*)sink, 1ull);  // keeps the loads live
+}
+
+__global__ void chase_kernel(const int64_t* __restrict__ src, int64_t steps, uint64_t* cycles) {
+    int64_t p = 0;
+    const long long t0 = clock64();
+    for (int64_t s = 0; s < steps; ++s) {
+        int64_t nx;
+        asm volatile("ld.global.cv.s64 %0, [%1];" : "=l"(nx) : "l"(src + p));
+        p = nx;
+    }
+    const long long t1 = clock64();
+    cycles[0] = (uint64_t)(t1 - t0);
+    cycles[1] = (uint64_t)p;
+}
+
+}  // namespace
+
+using namespace dgz;
+
+extern "C" dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32_t sm_count, int32_t warps, int32_t unroll,
+                                       uint64_t* sink_dev, dgz_stream stream) {
+    DGZ_REQUIRE(src_dev && sink_dev && bytes > 0 && bytes % 16 == 0 && ((uintptr_t)src_dev % 16) == 0, "dgz_probe_stream: bad args");
+    const int nsm = sm_count_of_current_device();
+    const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
+    if (warps <= 0 || warps > 32) warps = 32;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t chunks = bytes / 16;
+    switch (unroll) {
+        case 1: stream_kernel<1><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        case 2: stream_kernel<2><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        case 4: stream_kernel<4><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        case 16: stream_kernel<16><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        default: stream_kernel<8><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+    }
+    return launch_check("stream_kernel");
+}
+
+extern "C" dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream) {
+    DGZ_REQUIRE(src_dev && cycles_dev && steps > 0, "dgz_probe_chase: bad args");
+    chase_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const int64_t*)src_dev, steps, cycles_dev);
+    return launch_check("chase_kernel");
+}

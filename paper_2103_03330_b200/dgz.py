@@ -1,0 +1,332 @@
+"""Thin Python binding of libdgz (include/dgz.h): argument marshalling only.
+
+Every step of the hot path runs in libdgz's CUDA kernels; PyTorch supplies device memory,
+pinned host buffers and streams.  There is no CPU or PyTorch fallback: if ``libdgz.so`` is
+missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libdgz.so")
+
+if not os.path.exists(_SO):
+    raise ImportError(f"{_SO} is missing: build it with `python -m paper_2103_03330_b200.build` "
+                      "(no CPU fallback exists by design)")
+
+_lib = ctypes.CDLL(_SO)
+
+# --- constants (dgz.h) -------------------------------------------------------------------------
+OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_RANGE, ERR_STATE = range(6)
+F32, F16, BF16, U8 = range(4)
+REG_PORTABLE, REG_READONLY, REG_NO_PIN = 1, 2, 4
+HOST_HUGEPAGE, HOST_POPULATE = 1, 2
+GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
+MAX_FANOUT, MAX_LAYERS = 64, 8
+ELEM_BYTES = {F32: 4, F16: 2, BF16: 2, U8: 1}
+TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16, U8: torch.uint8}
+
+_STATUS = {0: "OK", 1: "INVALID", 2: "CUDA", 3: "NOMEM", 4: "RANGE", 5: "STATE"}
+
+
+class DgzError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: DGZ_ERR_{_STATUS.get(status, status)}: {last_error()}")
+
+
+class RangeError(DgzError, IndexError):
+    pass
+
+
+def _check(st: int, where: str) -> None:
+    if st != OK:
+        raise (RangeError if st == ERR_RANGE else DgzError)(st, where)
+
+
+# --- structs -----------------------------------------------------------------------------------
+class TableInfo(ctypes.Structure):
+    _fields_ = [("dev_ptr", ctypes.c_void_p), ("rows", ctypes.c_int64), ("dim", ctypes.c_int64),
+                ("row_bytes", ctypes.c_int64), ("elem_bytes", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("base_mod128", ctypes.c_int32), ("flags", ctypes.c_int32), ("pinned_bytes", ctypes.c_int64),
+                ("gpu_mem_delta", ctypes.c_int64), ("register_seconds", ctypes.c_double)]
+
+
+class GatherCfg(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("sm_count", ctypes.c_int32),
+                ("warps_per_cta", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int64), ("offsets", ctypes.c_void_p), ("cols", ctypes.c_void_p),
+                ("cols_is64", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class SampleOut(ctypes.Structure):
+    _fields_ = [("ids", ctypes.c_void_p), ("ids_cap", ctypes.c_int64), ("sizes_dev", ctypes.c_void_p),
+                ("sizes_host", ctypes.c_void_p), ("nbr", ctypes.c_void_p), ("nbr_local", ctypes.c_void_p),
+                ("cnt", ctypes.c_void_p), ("blocks_cap", ctypes.c_int64), ("cnt_cap", ctypes.c_int64),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+
+
+_vp, _i64, _i32, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
+                                    ctypes.c_uint32, ctypes.c_size_t)
+_P = ctypes.POINTER
+
+_SIGS = {
+    "dgz_abi_version": ([], ctypes.c_int),
+    "dgz_last_error": ([], ctypes.c_char_p),
+    "dgz_device_sm_count": ([], ctypes.c_int),
+    "dgz_host_alloc": ([ctypes.c_char_p, _sz, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
+    "dgz_host_free": ([_vp, _sz], ctypes.c_int),
+    "dgz_host_unlink": ([ctypes.c_char_p], ctypes.c_int),
+    "dgz_register_table": ([_vp, _i64, _i64, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
+    "dgz_unregister_table": ([_vp], ctypes.c_int),
+    "dgz_table_get_info": ([_vp, _P(TableInfo)], ctypes.c_int),
+    "dgz_gather": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
+    "dgz_gather_i32": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
+    "dgz_gather_ex": ([_vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
+    "dgz_check_errors": ([_vp, _vp], ctypes.c_int),
+    "dgz_sample_bounds": ([_i64, _i64, _P(_i32), ctypes.c_int, _P(_i64), _P(_i64), _P(_i64)], ctypes.c_int),
+    "dgz_sample_workspace_bytes": ([_i64, _i64, _P(_sz)], ctypes.c_int),
+    "dgz_sample_uniform": ([_P(Csr), _vp, _i64, _P(_i32), ctypes.c_int, _u64, _P(SampleOut), _vp], ctypes.c_int),
+    "dgz_sample_check": ([_P(SampleOut), _vp], ctypes.c_int),
+    "dgz_aggregate_mean": ([_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _i32, _vp], ctypes.c_int),
+    "dgz_probe_stream": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
+    "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTS = tuple(_SIGS)
+
+
+def abi_version() -> int:
+    return _lib.dgz_abi_version()
+
+
+def last_error() -> str:
+    m = _lib.dgz_last_error()
+    return m.decode() if m else ""
+
+
+def device_sm_count() -> int:
+    return _lib.dgz_device_sm_count()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _dptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return t.data_ptr()
+
+
+# --- host table manager ------------------------------------------------------------------------
+class HostBuffer:
+    """Host mapping from dgz_host_alloc (anonymous or /dev/shm shared)."""
+
+    def __init__(self, nbytes: int, shm_name: str | None = None, create: bool = True, flags: int = HOST_HUGEPAGE):
+        p = _vp()
+        name = shm_name.encode() if shm_name else None
+        _check(_lib.dgz_host_alloc(name, nbytes, int(create), flags, ctypes.byref(p)), "dgz_host_alloc")
+        self.ptr = p.value
+        self.nbytes = nbytes
+        self.shm_name = shm_name
+
+    def numpy(self, offset: int = 0, nbytes: int | None = None):
+        import numpy as np
+        n = self.nbytes - offset if nbytes is None else nbytes
+        buf = (ctypes.c_uint8 * n).from_address(self.ptr + offset)
+        return np.frombuffer(buf, dtype=np.uint8)
+
+    def free(self) -> None:
+        if self.ptr:
+            _check(_lib.dgz_host_free(self.ptr, self.nbytes), "dgz_host_free")
+            self.ptr = 0
+
+    def unlink(self) -> None:
+        if self.shm_name:
+            _check(_lib.dgz_host_unlink(self.shm_name.encode()), "dgz_host_unlink")
+
+
+def host_unlink(shm_name: str) -> None:
+    _check(_lib.dgz_host_unlink(shm_name.encode()), "dgz_host_unlink")
+
+
+# --- table registration ------------------------------------------------------------------------
+class Table:
+    """A registered (pinned + mapped) host feature table: the paper's unified tensor."""
+
+    def __init__(self, host_ptr: int, rows: int, dim: int, dtype: int = F32, flags: int = 0):
+        h = _vp()
+        _check(_lib.dgz_register_table(host_ptr, rows, dim, dtype, flags, ctypes.byref(h)), "dgz_register_table")
+        self.handle = h.value
+        self.dtype = dtype
+        self.info = self.get_info()
+
+    def get_info(self) -> TableInfo:
+        info = TableInfo()
+        _check(_lib.dgz_table_get_info(self.handle, ctypes.byref(info)), "dgz_table_get_info")
+        return info
+
+    @property
+    def rows(self) -> int:
+        return self.info.rows
+
+    @property
+    def row_bytes(self) -> int:
+        return self.info.row_bytes
+
+    def unregister(self) -> None:
+        if self.handle:
+            _check(_lib.dgz_unregister_table(self.handle), "dgz_unregister_table")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.unregister()
+        except Exception:
+            pass
+
+
+def register_table(host_ptr: int, rows: int, dim: int, dtype: int = F32, flags: int = 0) -> Table:
+    return Table(host_ptr, rows, dim, dtype, flags)
+
+
+def unregister_table(t: Table) -> None:
+    t.unregister()
+
+
+# --- gather ------------------------------------------------------------------------------------
+def gather_cfg(variant: int = GATHER_AUTO, sm_count: int = 0, warps_per_cta: int = 0, ctas_per_sm: int = 0) -> GatherCfg:
+    return GatherCfg(variant, sm_count, warps_per_cta, ctas_per_sm)
+
+
+def gather(table: Table, idx: torch.Tensor, out: torch.Tensor, n: int | None = None, n_dev: torch.Tensor | None = None,
+           cfg: GatherCfg | None = None, stream=None) -> torch.Tensor:
+    """out[r] = table[idx[r]] for r < n (or < min(n, *n_dev)); asynchronous on ``stream``."""
+    n = idx.numel() if n is None else n
+    assert out.numel() * out.element_size() >= n * table.row_bytes, "out too small"
+    s = _stream(stream)
+    if idx.dtype == torch.int32 and n_dev is None and cfg is None:
+        _check(_lib.dgz_gather_i32(table.handle, _dptr(idx), n, _dptr(out), s), "dgz_gather_i32")
+        return out
+    assert idx.dtype == torch.int64, "idx must be int64 (or int32 with the default config)"
+    if n_dev is None and cfg is None:
+        _check(_lib.dgz_gather(table.handle, _dptr(idx), n, _dptr(out), s), "dgz_gather")
+    else:
+        _check(_lib.dgz_gather_ex(table.handle, _dptr(idx), n, _dptr(n_dev), _dptr(out),
+                                  ctypes.byref(cfg) if cfg is not None else None, s), "dgz_gather_ex")
+    return out
+
+
+def check_errors(table: Table, stream=None) -> None:
+    _check(_lib.dgz_check_errors(table.handle, _stream(stream)), "dgz_check_errors")
+
+
+# --- sampler -----------------------------------------------------------------------------------
+def _i32arr(xs):
+    return (ctypes.c_int32 * max(len(xs), 1))(*xs)
+
+
+def sample_bounds(n_nodes: int, n_seeds: int, fanouts) -> tuple:
+    fan = _i32arr(list(fanouts))
+    L = len(fanouts)
+    b = (ctypes.c_int64 * (L + 1))()
+    be, ce = _i64(), _i64()
+    _check(_lib.dgz_sample_bounds(n_nodes, n_seeds, fan, L, b, ctypes.byref(be), ctypes.byref(ce)), "dgz_sample_bounds")
+    return list(b), be.value, ce.value
+
+
+def sample_workspace_bytes(n_nodes: int, max_seeds: int) -> int:
+    v = _sz()
+    _check(_lib.dgz_sample_workspace_bytes(n_nodes, max_seeds, ctypes.byref(v)), "dgz_sample_workspace_bytes")
+    return v.value
+
+
+class SampleBuffers:
+    """Caller-owned outputs + workspace of dgz_sample_uniform, sized by dgz_sample_bounds."""
+
+    def __init__(self, n_nodes: int, max_seeds: int, fanouts, device=None, blocks: bool = True, local: bool = True):
+        device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.fanouts = tuple(int(f) for f in fanouts)
+        self.bounds, be, ce = sample_bounds(n_nodes, max_seeds, self.fanouts)
+        L = len(self.fanouts)
+        self.ids = torch.empty(max(self.bounds[-1], 1), dtype=torch.int64, device=device)
+        self.sizes_dev = torch.zeros(L + 1, dtype=torch.int64, device=device)
+        self.sizes_host = torch.zeros(L + 1, dtype=torch.int64).pin_memory()
+        self.nbr = torch.empty(max(be, 1), dtype=torch.int64, device=device) if blocks else None
+        self.cnt = torch.empty(max(ce, 1), dtype=torch.int32, device=device) if blocks else None
+        self.local = torch.empty(max(be, 1), dtype=torch.int32, device=device) if (blocks and local) else None
+        wsb = sample_workspace_bytes(n_nodes, max_seeds)
+        self.workspace = torch.empty(wsb, dtype=torch.uint8, device=device)
+        self.struct = SampleOut(self.ids.data_ptr(), self.ids.numel(), self.sizes_dev.data_ptr(), self.sizes_host.data_ptr(),
+                                _dptr(self.nbr), _dptr(self.local), _dptr(self.cnt), be, ce,
+                                self.workspace.data_ptr(), wsb)
+
+    def hop_blocks(self, sizes=None):
+        """Per-hop (nbr [n_k x f_k], cnt [n_k], local [n_k x f_k]) views (after a sync)."""
+        sizes = self.sizes_host.tolist() if sizes is None else sizes
+        out, nb, cb = [], 0, 0
+        for k, f in enumerate(self.fanouts):
+            nk = sizes[k]
+            out.append((self.nbr[nb:nb + nk * f].view(nk, f), self.cnt[cb:cb + nk],
+                        self.local[nb:nb + nk * f].view(nk, f) if self.local is not None else None))
+            nb += self.bounds[k] * f
+            cb += self.bounds[k]
+        return out
+
+
+class Graph:
+    """CSR in HBM (dgz_csr)."""
+
+    def __init__(self, offsets: torch.Tensor, cols: torch.Tensor):
+        assert offsets.dtype == torch.int64 and cols.dtype in (torch.int32, torch.int64)
+        self.offsets, self.cols = offsets, cols
+        self.n_nodes = offsets.numel() - 1
+        self.struct = Csr(self.n_nodes, offsets.data_ptr(), cols.data_ptr(), int(cols.dtype == torch.int64), 0)
+
+
+def sample_uniform(graph: Graph, seeds: torch.Tensor, fanouts, rng_seed: int, bufs: SampleBuffers, stream=None) -> SampleBuffers:
+    assert seeds.dtype == torch.int64
+    fan = _i32arr(list(fanouts))
+    _check(_lib.dgz_sample_uniform(ctypes.byref(graph.struct), _dptr(seeds), seeds.numel(), fan, len(fanouts),
+                                   rng_seed & (2**64 - 1), ctypes.byref(bufs.struct), _stream(stream)),
+           "dgz_sample_uniform")
+    return bufs
+
+
+def sample_check(bufs: SampleBuffers, stream=None) -> None:
+    _check(_lib.dgz_sample_check(ctypes.byref(bufs.struct), _stream(stream)), "dgz_sample_check")
+
+
+# --- stand-in consumer, probes -------------------------------------------------------------------
+def aggregate_mean(x: torch.Tensor, dim: int, nbr_local: torch.Tensor, cnt: torch.Tensor, fanout: int,
+                   n_dst_dev: torch.Tensor | None, n_dst_max: int, y: torch.Tensor, repeat: int = 1, sm_count: int = 0,
+                   stream=None) -> torch.Tensor:
+    _check(_lib.dgz_aggregate_mean(_dptr(x), dim, _dptr(nbr_local), _dptr(cnt), fanout, _dptr(n_dst_dev), n_dst_max,
+                                   _dptr(y), repeat, sm_count, _stream(stream)), "dgz_aggregate_mean")
+    return y
+
+
+def probe_stream(src_dev_ptr: int, nbytes: int, sm_count: int, warps: int, unroll: int, sink: torch.Tensor, stream=None):
+    _check(_lib.dgz_probe_stream(src_dev_ptr, nbytes, sm_count, warps, unroll, _dptr(sink), _stream(stream)),
+           "dgz_probe_stream")
+
+
+def probe_chase(src_dev_ptr: int, steps: int, cycles: torch.Tensor, stream=None):
+    _check(_lib.dgz_probe_chase(src_dev_ptr, steps, _dptr(cycles), _stream(stream)), "dgz_probe_chase")

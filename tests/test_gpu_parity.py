@@ -1,0 +1,260 @@
+"""CUDA path (libdgz through its C ABI) vs the CPU oracle, element by element.
+
+Bar: bit-exact (the gather moves bytes; the sampler is integer work).  Inputs come from
+dgz_inputs; expected values come only from ``oracle``.
+"""
+import numpy as np
+import pytest
+import torch
+
+import dgz_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2103_03330_b200 import dgz
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    return torch.device("cuda", 0)
+
+
+class HostTable:
+    """A host table at byte offset `base` inside a page-aligned mapping, registered."""
+
+    def __init__(self, rows, row_bytes, seed, base=0, dtype=None, flags=0):
+        dtype = dgz.U8 if dtype is None else dtype
+        eb = dgz.ELEM_BYTES[dtype]
+        assert row_bytes % eb == 0 and base % eb == 0
+        self.rows, self.R, self.base = rows, row_bytes, base
+        self.buf = dgz.HostBuffer(rows * row_bytes + base + 4096)
+        arr = self.buf.numpy()
+        gen.fill_table(arr.ctypes.data + base, rows * row_bytes, seed)
+        self.np = arr[base:base + rows * row_bytes]
+        self.table = dgz.register_table(self.buf.ptr + base, rows, row_bytes // eb, dtype, flags)
+
+    def close(self):
+        self.table.unregister()
+        self.buf.free()
+
+
+def _gather_dev(t, idx_np, cfg=None, out_offset=0, idx_dtype=torch.int64, n_dev=None, fill=0xAB):
+    n = idx_np.shape[0]
+    R = t.R
+    raw = torch.full((n * R + 64,), fill, dtype=torch.uint8, device="cuda")
+    out = raw[out_offset:out_offset + n * R]
+    idx = torch.from_numpy(np.ascontiguousarray(idx_np)).to(device="cuda", dtype=idx_dtype)
+    dgz.gather(t.table, idx, out, n=n, n_dev=n_dev, cfg=cfg)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().reshape(n, R) if n else np.zeros((0, R), np.uint8)
+
+
+VARIANTS = [dgz.GATHER_SEGMENT, dgz.GATHER_BULK, dgz.GATHER_NAIVE, dgz.GATHER_SHIFT] if torch.cuda.is_available() else []
+
+
+@pytest.mark.parametrize("R", gen.SWEEP_ROW_BYTES)
+@pytest.mark.parametrize("base", gen.SWEEP_BASE_OFFSETS)
+def test_gather_sweep_segment(dev, R, base):
+    rows = max(64, min(4000, (8 << 20) // R))
+    t = HostTable(rows, R, seed=R * 131 + base, base=base)
+    try:
+        idx = gen.random_ids(rows, 1000 + 17, seed=R + base)   # ragged tail (not a multiple of 32)
+        want, bad = oracle.gather(t.np, R, idx)
+        assert bad == 0
+        got = _gather_dev(t, idx)
+        assert np.array_equal(got, want)
+    finally:
+        t.close()
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
+@pytest.mark.parametrize("R,base", [(512, 0), (400, 0), (2408, 0), (1028, 4), (100, 64), (16, 8), (4096, 16), (1044, 0)])
+def test_gather_variants(dev, variant, R, base):
+    rows = 3000
+    t = HostTable(rows, R, seed=7 + R, base=base, dtype=dgz.F32)
+    try:
+        idx = gen.random_ids(rows, 777, seed=R)
+        want, _ = oracle.gather(t.np, R, idx)
+        for off in (0, 4, 8):
+            got = _gather_dev(t, idx, cfg=dgz.gather_cfg(variant=variant), out_offset=off)
+            assert np.array_equal(got, want), (variant, off)
+    finally:
+        t.close()
+
+
+@pytest.mark.parametrize("dtype,dim", [("F16", 33), ("F16", 101), ("BF16", 64), ("U8", 37), ("U8", 3), ("F32", 1)])
+def test_gather_dtypes_odd_rows(dev, dtype, dim):
+    d = getattr(dgz, dtype)
+    R = dim * dgz.ELEM_BYTES[d]
+    rows = 2000
+    t = HostTable(rows, R, seed=dim, base=dgz.ELEM_BYTES[d] * 3, dtype=d)
+    try:
+        idx = gen.random_ids(rows, 555, seed=dim)
+        want, _ = oracle.gather(t.np, R, idx)
+        for variant in (1, 4, 2, 3):
+            for off in (0, dgz.ELEM_BYTES[d]):
+                got = _gather_dev(t, idx, cfg=dgz.gather_cfg(variant=variant), out_offset=off)
+                assert np.array_equal(got, want), (variant, off)
+    finally:
+        t.close()
+
+
+def test_gather_edge_cases(dev):
+    R, rows = 520, 1000
+    t = HostTable(rows, R, seed=3)
+    try:
+        # n = 0 is a no-op
+        assert _gather_dev(t, np.zeros(0, np.int64)).shape == (0, R)
+        # n = 1, first and last row (span ends at the registered range), duplicates, int32 IDs
+        for idx in (np.array([0]), np.array([rows - 1]), np.array([5, 5, 5, rows - 1, 0, 5])):
+            want, _ = oracle.gather(t.np, R, idx)
+            assert np.array_equal(_gather_dev(t, idx), want)
+            assert np.array_equal(_gather_dev(t, idx, idx_dtype=torch.int32), want)
+        # device-resident count: only the first m rows are written
+        idx = gen.random_ids(rows, 300, 1)
+        n_dev = torch.tensor([123], dtype=torch.int64, device="cuda")
+        got = _gather_dev(t, idx, n_dev=n_dev, cfg=dgz.gather_cfg())
+        want, _ = oracle.gather(t.np, R, idx[:123])
+        assert np.array_equal(got[:123], want) and (got[123:] == 0xAB).all()
+        # bounded persistent grids (the SM-partition knob) give the same bytes
+        want, _ = oracle.gather(t.np, R, idx)
+        for k in (1, 2, 8, 148):
+            for variant in (1, 4):
+                assert np.array_equal(_gather_dev(t, idx, cfg=dgz.gather_cfg(variant=variant, sm_count=k)), want)
+    finally:
+        t.close()
+
+
+def test_gather_out_of_range_is_latched(dev):
+    R, rows = 256, 100
+    t = HostTable(rows, R, seed=4)
+    try:
+        idx = np.array([1, rows, 2, -1, rows - 1], dtype=np.int64)
+        for variant in (1, 4, 2):
+            got = _gather_dev(t, idx, cfg=dgz.gather_cfg(variant=variant))
+            with pytest.raises(dgz.RangeError):
+                dgz.check_errors(t.table)
+            dgz.check_errors(t.table)  # the flag is cleared by the check
+            want, _ = oracle.gather(t.np, R, idx)
+            for r in (0, 2, 4):
+                assert np.array_equal(got[r], want[r])
+            assert (got[1] == 0xAB).all() and (got[3] == 0xAB).all()
+    finally:
+        t.close()
+
+
+def test_gather_invalid_args(dev):
+    t = HostTable(10, 64, seed=1, dtype=dgz.F32)
+    try:
+        idx = torch.zeros(4, dtype=torch.int64, device="cuda")
+        out = torch.empty(4 * 64 + 4, dtype=torch.uint8, device="cuda")
+        with pytest.raises(dgz.DgzError) as e:
+            dgz.gather(t.table, idx, out[1:], n=4)  # not aligned to the fp32 element
+        assert e.value.status == dgz.ERR_INVALID
+        with pytest.raises(dgz.DgzError) as e:
+            dgz.gather(t.table, idx, out, n=-1)
+        assert e.value.status == dgz.ERR_INVALID
+    finally:
+        t.close()
+
+
+def test_registration_info(dev):
+    t = HostTable(1000, 512, seed=2, base=64)
+    try:
+        info = t.table.info
+        assert info.rows == 1000 and info.row_bytes == 512 and info.base_mod128 == 64 and info.elem_bytes == 1
+        assert info.pinned_bytes >= 1000 * 512
+    finally:
+        t.close()
+
+
+# ------------------------------------------------------------------------------------------------
+# sampler parity
+# ------------------------------------------------------------------------------------------------
+def _sample_dev(off, col, seeds, fanouts, rng_seed, col64=False):
+    g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col.astype(np.int64 if col64 else np.int32)).cuda())
+    bufs = dgz.SampleBuffers(g.n_nodes, max(len(seeds), 1), fanouts)
+    s = torch.from_numpy(np.asarray(seeds, dtype=np.int64)).cuda()
+    dgz.sample_uniform(g, s, fanouts, rng_seed, bufs)
+    torch.cuda.synchronize()
+    return g, bufs
+
+
+def _compare_plan(off, col, seeds, fanouts, rng_seed, col64=False):
+    want = oracle.sample_uniform(off, col, seeds, fanouts, rng_seed)
+    g, bufs = _sample_dev(off, col, seeds, fanouts, rng_seed, col64)
+    sizes = bufs.sizes_host.tolist()
+    assert sizes == want.sizes.tolist()
+    assert bufs.sizes_dev.cpu().tolist() == sizes
+    assert np.array_equal(bufs.ids[:sizes[-1]].cpu().numpy(), want.U)
+    for k, (nbr, cnt, loc) in enumerate(bufs.hop_blocks()):
+        assert np.array_equal(cnt.cpu().numpy(), want.cnt[k])
+        assert np.array_equal(nbr.cpu().numpy(), want.nbr[k])
+        assert np.array_equal(loc.cpu().numpy(), want.local[k])
+    return want, bufs
+
+
+@pytest.mark.parametrize("cid", [1])
+def test_sampler_config1_many_batches(dev, cid):
+    c = gen.CONFIGS[cid]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    for j in range(12):  # crosses an epoch boundary (10 batches per epoch), short last batch
+        seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
+        _compare_plan(off, col, seeds, c.fanouts, gen.batch_rng_seed(c.seed, j))
+
+
+@pytest.mark.parametrize("n,deg,fan", [(20_000, 50.5, (15, 10, 5)), (5_000, 492.0, (25, 10)), (300_000, 14.4, (15, 10, 5)),
+                                       (1000, 3.0, (64, 1, 0, 2)), (70_000, 8.0, ())])
+def test_sampler_shapes(dev, n, deg, fan):
+    off, col = gen.gen_csr(n, deg, n)
+    seeds = gen.batch_seeds(n, 1024 if n > 1024 else n // 2, n, 3)
+    _compare_plan(off, col, seeds, fan, gen.batch_rng_seed(n, 3))
+    _compare_plan(off, col, seeds, fan, gen.batch_rng_seed(n, 3), col64=True)
+
+
+def test_sampler_seed_cases(dev):
+    off, col = gen.gen_csr(3000, 6.0, 5)
+    _compare_plan(off, col, [7, 3, 7, 9, 3, 2999, 0], (4, 3), 99)      # duplicates: first kept
+    _compare_plan(off, col, [1], (10,), 5)
+    # n_seeds = 0
+    g, bufs = _sample_dev(off, col, [], (3, 2), 1)
+    assert bufs.sizes_host.tolist() == [0, 0, 0]
+    # out-of-range seed: latched, reported by dgz_sample_check, the seed is dropped
+    g, bufs = _sample_dev(off, col, [5, 3000, 6], (2,), 1)
+    with pytest.raises(dgz.RangeError):
+        dgz.sample_check(bufs)
+    assert bufs.ids[:2].cpu().tolist() == [5, 6]
+
+
+def test_sampler_isolated_and_large_seed_set(dev):
+    off = np.zeros(50_001, dtype=np.int64)
+    col = np.zeros(0, dtype=np.int32)
+    _compare_plan(off, col, gen.batch_seeds(50_000, 9000, 1, 0), (5, 5), 3)
+    off, col = gen.gen_csr(200_000, 4.0, 8)
+    _compare_plan(off, col, gen.batch_seeds(200_000, 20_000, 8, 1), (3, 2), 4)   # > one seed chunk
+
+
+def test_sample_then_gather_device_count(dev):
+    """The step as the bench runs it: sampler -> gather with the device-resident |U|."""
+    c = gen.CONFIGS[1]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, 0)
+        rs = gen.batch_rng_seed(c.seed, 0)
+        g, bufs = _sample_dev(off, col, seeds, c.fanouts, rs)
+        L = len(c.fanouts)
+        out = torch.empty(bufs.bounds[-1] * c.row_bytes, dtype=torch.uint8, device="cuda")
+        dgz.gather(t.table, bufs.ids, out, n=bufs.bounds[-1], n_dev=bufs.sizes_dev[L:L + 1], cfg=dgz.gather_cfg())
+        torch.cuda.synchronize()
+        want = oracle.sample_uniform(off, col, seeds, c.fanouts, rs, with_blocks=False)
+        n = want.U.shape[0]
+        exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+        assert np.array_equal(out[:n * c.row_bytes].cpu().numpy().reshape(n, -1), exp)
+    finally:
+        t.close()
