@@ -64,6 +64,10 @@ DGZ_API int dgz_device_sm_count(void);
  * ========================================================================================== */
 #define DGZ_HOST_HUGEPAGE 1u /* madvise(MADV_HUGEPAGE) on the mapping */
 #define DGZ_HOST_POPULATE 2u /* pre-fault every page at creation */
+#define DGZ_HOST_VMM 4u      /* CUDA VMM host allocation (cuMemCreate on host NUMA node 0): pinned,
+                                CPU-accessible, mapped into the current GPU with large pages at the
+                                same address.  Needs a CUDA device; shm_name must be NULL (share it
+                                across processes with dgz_host_export / dgz_host_import). */
 
 /* Map `bytes` of host memory.  shm_name == NULL: private anonymous mapping.  Otherwise a POSIX
  * shared-memory object (/dev/shm/<name>): create != 0 creates/truncates it to `bytes`,
@@ -72,6 +76,13 @@ DGZ_API int dgz_device_sm_count(void);
 DGZ_API dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int create, uint32_t flags, void** ptr);
 DGZ_API dgz_status dgz_host_free(void* ptr, size_t bytes);
 DGZ_API dgz_status dgz_host_unlink(const char* shm_name);
+/* POSIX file descriptor of a DGZ_HOST_VMM allocation (ptr = the address dgz_host_alloc returned);
+ * pass it to another process (SCM_RIGHTS / pidfd_getfd) and map it there with dgz_host_import.
+ * The caller closes the fd. */
+DGZ_API dgz_status dgz_host_export(void* ptr, int* fd);
+/* Map an exported DGZ_HOST_VMM allocation of `bytes` bytes into this process, accessible by the
+ * CPU and the current device.  Release with dgz_host_free. */
+DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 
 /* ==========================================================================================
  * Table registration (step a1).  The paper's "unified tensor": cudaHostRegister page-locks
@@ -81,6 +92,8 @@ DGZ_API dgz_status dgz_host_unlink(const char* shm_name);
 #define DGZ_REG_PORTABLE 1u  /* cudaHostRegisterPortable: valid on every device of this process */
 #define DGZ_REG_READONLY 2u  /* cudaHostRegisterReadOnly when the device supports it */
 #define DGZ_REG_NO_PIN 4u    /* memory is already page-locked (e.g. cudaHostAlloc): map only */
+#define DGZ_REG_VMM_BACKED 8u /* (reported in dgz_table_info.flags) the table lies in a DGZ_HOST_VMM
+                                 allocation: no cudaHostRegister, large-page GPU mapping */
 
 /* host_ptr: row 0 of a row-major, unpadded rows x dim table of `dtype` elements in host
  * memory (any alignment; unaligned bases are a first-class case, S:37 base_offset).  The caller
@@ -126,12 +139,21 @@ typedef enum {
     DGZ_GATHER_BULK = 4     /* cp.async.bulk (TMA engine) row copies via shared memory */
 } dgz_gather_variant;
 
+typedef enum {
+    DGZ_SCHED_AUTO = 0,        /* = INTERLEAVED (measured best on B200) */
+    DGZ_SCHED_INTERLEAVED = 1, /* warp w of the grid takes 32-row batches w, w + W, ... */
+    DGZ_SCHED_BLOCKED = 2      /* CTA c owns a contiguous range of batches (translation-aware:
+                                  with a sorted index list each SM walks its own address range) */
+} dgz_gather_schedule;
+
 typedef struct {
     int32_t variant;       /* dgz_gather_variant */
-    int32_t sm_count;      /* 0 = every SM; k > 0 bounds the persistent grid to k CTAs, one per
-                              SM (the B200 analogue of the paper's MPS X%, step a6) */
+    int32_t sm_count;      /* 0 = default grid; k > 0 bounds the persistent grid to k CTAs, one
+                              per SM (the B200 analogue of the paper's MPS X%, step a6) */
     int32_t warps_per_cta; /* 0 = default */
-    int32_t ctas_per_sm;   /* 0 = default (1 when sm_count > 0) */
+    int32_t ctas_per_sm;   /* 0 = default (1) */
+    int32_t schedule;      /* dgz_gather_schedule */
+    int32_t reserved;
 } dgz_gather_cfg;
 
 /* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
@@ -139,6 +161,14 @@ typedef struct {
  * same stream without a host round trip.  cfg may be NULL (defaults). */
 DGZ_API dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n, const int64_t* n_dev,
                          void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream);
+
+/* Gather in a caller-chosen processing order: out[dst_pos[k]] = table[idx[k]] for k < n (or
+ * < min(n, *n_dev)).  With idx sorted by address and dst_pos its inverse permutation this is
+ * the same result as dgz_gather on the unsorted list, fetched in table order (each SM walks a
+ * contiguous address range: far fewer GPU address-translation misses on tables of tens of GB;
+ * DESIGN.md section 5).  dst_pos must be a permutation of [0, n) (else rows may overlap). */
+DGZ_API dgz_status dgz_gather_perm(dgz_table t, const int64_t* idx_dev, const int64_t* dst_pos_dev, int64_t n,
+                                   const int64_t* n_dev, void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream);
 
 /* Synchronises `stream`, reads and clears the table's device RANGE flag for the current
  * device: DGZ_ERR_RANGE if any gather since the last check met an out-of-range ID. */
@@ -178,6 +208,9 @@ typedef struct {
     int64_t cnt_cap;       /* elements available in cnt */
     void* workspace;       /* device scratch of dgz_sample_workspace_bytes() bytes; not */
     size_t workspace_bytes;/* shared between calls that may run concurrently */
+    int64_t* ids_sorted;   /* optional device [ids_cap]: the IDs of `ids` in ascending order */
+    int64_t* ids_sorted_pos; /* optional device [ids_cap] (with ids_sorted): position in `ids` of
+                              each sorted ID -- the inputs of dgz_gather_perm */
 } dgz_sample_out;
 
 /* bounds[k] = min(n_nodes, n_seeds * prod_{i<k}(1 + fanouts[i])) for k = 0..L; also the

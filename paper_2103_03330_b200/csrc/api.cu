@@ -47,6 +47,10 @@ static double now_s() {
 
 using namespace dgz;
 
+dgz_status dgz_vmm_alloc(size_t bytes, void** ptr);
+int dgz_vmm_free(void* ptr);
+int dgz_vmm_register(const void* p, size_t bytes);
+
 extern "C" int dgz_abi_version(void) { return DGZ_ABI_VERSION; }
 extern "C" const char* dgz_last_error(void) { return g_err; }
 extern "C" int dgz_device_sm_count(void) { return sm_count_of_current_device(); }
@@ -57,6 +61,10 @@ extern "C" int dgz_device_sm_count(void) { return sm_count_of_current_device(); 
 extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int create, uint32_t flags, void** ptr) {
     DGZ_REQUIRE(ptr && bytes > 0, "dgz_host_alloc: null ptr or zero size");
     *ptr = nullptr;
+    if (flags & DGZ_HOST_VMM) {
+        DGZ_REQUIRE(!shm_name, "dgz_host_alloc: DGZ_HOST_VMM allocations are shared with dgz_host_export, not by name");
+        return dgz_vmm_alloc(bytes, ptr);
+    }
     void* p = MAP_FAILED;
     if (!shm_name) {
         p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
@@ -94,6 +102,7 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
 
 extern "C" dgz_status dgz_host_free(void* ptr, size_t bytes) {
     DGZ_REQUIRE(ptr && bytes > 0, "dgz_host_free: null ptr or zero size");
+    if (dgz_vmm_free(ptr) == 1) return DGZ_OK;
     if (munmap(ptr, bytes) != 0) { set_error("munmap: %s", strerror(errno)); return DGZ_ERR_INVALID; }
     return DGZ_OK;
 }
@@ -151,7 +160,14 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
     size_t free0 = 0, free1 = 0, total = 0;
     cudaMemGetInfo(&free0, &total);
     double t0 = now_s();
-    if (!(flags & DGZ_REG_NO_PIN)) {
+    const int vmm = dgz_vmm_register(host_ptr, bytes);
+    if (vmm < 0) {
+        delete t;
+        return (dgz_status)(-vmm);
+    }
+    if (vmm == 1) {
+        t->flags |= DGZ_REG_NO_PIN | DGZ_REG_VMM_BACKED;  // CUDA VMM host memory: already mapped
+    } else if (!(flags & DGZ_REG_NO_PIN)) {
         unsigned int rf = cudaHostRegisterMapped;
         if (flags & DGZ_REG_PORTABLE) rf |= cudaHostRegisterPortable;
         if (flags & DGZ_REG_READONLY) {
@@ -171,8 +187,8 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
         }
     }
     t->register_seconds = now_s() - t0;
-    void* dptr = nullptr;
-    e = cudaHostGetDevicePointer(&dptr, (void*)host_ptr, 0);
+    void* dptr = (void*)host_ptr;  // VMM host memory: one VA for the CPU and every GPU
+    e = vmm == 1 ? cudaSuccess : cudaHostGetDevicePointer(&dptr, (void*)host_ptr, 0);
     if (e != cudaSuccess) {
         if (t->reg_base) cudaHostUnregister(t->reg_base);
         delete t;

@@ -63,8 +63,8 @@ __device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo,
 template <int SW, int U, typename IdxT>
 __global__ void __launch_bounds__(1024, 1)
 gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
-                      int64_t n_cap, const int64_t* __restrict__ n_dev, uint8_t* __restrict__ dst,
-                      int* __restrict__ err) {
+                      const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
+                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked) {
     int64_t n = n_cap;
     if (n_dev) {
         const int64_t m = *n_dev;
@@ -73,22 +73,46 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
     const int lane = threadIdx.x & 31;
     const int g = lane >> 3;
     const int sub = lane & 7;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const uint64_t base = reinterpret_cast<uint64_t>(src);
     const uint64_t dbase = reinterpret_cast<uint64_t>(dst);
 
-    int64_t b0 = warp * 32;
-    // software-pipelined ID load: the next batch's ID is fetched before this batch's PCIe loads
-    int64_t id_next = -1;
-    if (b0 + lane < n) id_next = (int64_t)idx[b0 + lane];
+    // Schedule of 32-row batches.  Interleaved: warp w of the grid takes batches w, w + W, ...
+    // Blocked (translation-aware): CTA c owns a contiguous range of batches and its warps
+    // interleave inside it, so each SM walks its own address range monotonically when the
+    // index list is sorted (one GPU TLB miss per 2 MiB region per SM instead of per row).
+    const int64_t nb = (n + 31) >> 5;
+    const int wid = threadIdx.x >> 5;
+    const int wpc = blockDim.x >> 5;
+    int64_t bcur, bend, bstep;
+    if (blocked) {
+        const int64_t per = (nb + gridDim.x - 1) / gridDim.x;
+        bcur = int64_t(blockIdx.x) * per + wid;
+        bend = min(nb, int64_t(blockIdx.x + 1) * per);
+        bstep = wpc;
+    } else {
+        bcur = int64_t(blockIdx.x) * wpc + wid;
+        bend = nb;
+        bstep = int64_t(gridDim.x) * wpc;
+    }
 
-    for (; b0 < n; b0 += nwarps * 32) {
+    // software-pipelined ID load: the next batch's ID is fetched before this batch's PCIe loads
+    int64_t id_next = -1, dp_next = -1;
+    if (bcur < bend && (bcur << 5) + lane < n) {
+        id_next = (int64_t)idx[(bcur << 5) + lane];
+        dp_next = dst_pos ? dst_pos[(bcur << 5) + lane] : (bcur << 5) + lane;
+    }
+
+    for (; bcur < bend; bcur += bstep) {
+        const int64_t b0 = bcur << 5;
         const int64_t r = b0 + lane;
         int64_t id = id_next;
+        const int64_t drow = dp_next;
         {
-            const int64_t rn = r + nwarps * 32;
-            id_next = rn < n ? (int64_t)idx[rn] : -1;
+            const int64_t bn = bcur + bstep;
+            const int64_t rn = (bn << 5) + lane;
+            const bool ok = bn < bend && rn < n;
+            id_next = ok ? (int64_t)idx[rn] : -1;
+            dp_next = ok ? (dst_pos ? dst_pos[rn] : rn) : -1;
         }
         if (r < n && (id < 0 || id >= rows)) {
             atomicOr(err, 1);
@@ -124,7 +148,7 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                 const uint64_t ar = __shfl_sync(0xffffffffu, a, sl);
                 const int er = __shfl_sync(0xffffffffu, excl, sl);
                 // chunk = 16 B piece `sub` of line (t - er) of the row's 128 B-aligned segment list
-                const int q = (int)(ar & 127u);  // row start offset within its first line
+                const int q = (int)(ar & 127u);               // row start offset within its first line
                 const int cq = (t - er) * 128 + sub * 16 - q;  // chunk start relative to the row start
                 const bool act = (t < T) && (cq + 16 > 0) && (cq < (int)R);
                 pk[u] = act ? (((cq + 128) << 5) | sl) : -1;
@@ -132,10 +156,11 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
+                const int sl = pk[u] & 31;
+                const int64_t dr = __shfl_sync(0xffffffffu, drow, sl);
                 if (pk[u] >= 0) {
                     const int cq = (pk[u] >> 5) - 128;
-                    const int sl = pk[u] & 31;
-                    const uint64_t d = dbase + (uint64_t)(b0 + sl) * (uint64_t)R + (uint64_t)(int64_t)cq;
+                    const uint64_t d = dbase + (uint64_t)dr * (uint64_t)R + (uint64_t)(int64_t)cq;
                     store_pieces<SW>(d, v[u], cq < 0 ? -cq : 0, (int)R - cq > 16 ? 16 : (int)R - cq);
                 }
             }
@@ -184,22 +209,31 @@ gather_elem_kernel(const T* __restrict__ src, int64_t rows, int64_t F, const Idx
     }
 }
 
+struct SegLaunch {
+    const int64_t* dst_pos;
+    int64_t n;
+    const int64_t* n_dev;
+    uint8_t* out;
+    int* err;
+    int blocks, threads, blocked;
+    cudaStream_t s;
+};
+
 template <int SW, typename IdxT>
-cudaError_t launch_segment(const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, uint8_t* out, int* err,
-                           int blocks, int threads, cudaStream_t s) {
-    gather_segment_kernel<SW, 8, IdxT><<<blocks, threads, 0, s>>>(t->dev, t->rows, t->row_bytes, idx, n, n_dev, out, err);
+cudaError_t launch_segment(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
+    gather_segment_kernel<SW, 8, IdxT><<<L.blocks, L.threads, 0, L.s>>>(t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n,
+                                                                        L.n_dev, L.out, L.err, L.blocked);
     return cudaGetLastError();
 }
 
 template <typename IdxT>
-cudaError_t launch_segment_sw(int sw, const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, uint8_t* out,
-                              int* err, int blocks, int threads, cudaStream_t s) {
+cudaError_t launch_segment_sw(int sw, const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
     switch (sw) {
-        case 16: return launch_segment<16>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        case 8: return launch_segment<8>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        case 4: return launch_segment<4>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        case 2: return launch_segment<2>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        default: return launch_segment<1>(t, idx, n, n_dev, out, err, blocks, threads, s);
+        case 16: return launch_segment<16>(t, idx, L);
+        case 8: return launch_segment<8>(t, idx, L);
+        case 4: return launch_segment<4>(t, idx, L);
+        case 2: return launch_segment<2>(t, idx, L);
+        default: return launch_segment<1>(t, idx, L);
     }
 }
 
@@ -226,11 +260,11 @@ cudaError_t launch_elem(const dgz_table_s* t, const IdxT* idx, int64_t n, const 
 
 using namespace dgz;
 
-dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, int64_t n, const int64_t* n_dev, void* out,
-                           int* err, int sms, int warps, int ctas_per_sm, cudaStream_t s);
+dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n,
+                           const int64_t* n_dev, void* out, int* err, int sms, int warps, int blocked, cudaStream_t s);
 
-dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n, const int64_t* n_dev, void* out,
-                           const dgz_gather_cfg* cfg, cudaStream_t s) {
+dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n, const int64_t* n_dev,
+                           void* out, const dgz_gather_cfg* cfg, cudaStream_t s) {
     DGZ_REQUIRE(t, "dgz_gather: null table");
     DGZ_REQUIRE(n >= 0, "dgz_gather: n < 0");
     if (n == 0) return DGZ_OK;
@@ -244,7 +278,7 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n
     }
     int dev = 0;
     DGZ_CUDA(cudaGetDevice(&dev));
-    if (dev != t->device && !(t->flags & DGZ_REG_PORTABLE)) {
+    if (dev != t->device && !(t->flags & (DGZ_REG_PORTABLE | DGZ_REG_VMM_BACKED))) {
         set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
         return DGZ_ERR_STATE;
     }
@@ -252,13 +286,23 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n
     if (!err) { set_error("dgz_gather: cannot allocate the device flag"); return DGZ_ERR_CUDA; }
     const int nsm = sm_count_of_current_device();
     int variant = cfg ? cfg->variant : DGZ_GATHER_AUTO;
-    int k = (cfg && cfg->sm_count > 0) ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : nsm;
+    if (variant == DGZ_GATHER_AUTO) variant = DGZ_GATHER_SEGMENT;
     const bool bounded = cfg && cfg->sm_count > 0;
-    int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta : (bounded ? 32 : 16);
+    // Defaults measured on B200.  Unsorted lists: the whole GPU keeps as
+    // many rows in flight as possible to ride out GPU address-translation misses.  Sorted lists
+    // (dgz_gather_perm): a narrow in-flight window (~200 warps x 8 rows) keeps translations
+    // local and still covers the PCIe bandwidth-delay product; it also leaves SMs free.
+    const bool sorted_path = dst_pos != nullptr;
+    int k = bounded ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : (sorted_path && nsm > 96 ? 96 : nsm);
+    int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta
+                                                : (variant == DGZ_GATHER_BULK ? 8 : (sorted_path ? 2 : 16));
     if (warps > 32) warps = 32;
     int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : 1;
     if (warps * cps > 64) cps = 64 / warps > 0 ? 64 / warps : 1;
-    if (variant == DGZ_GATHER_AUTO) variant = DGZ_GATHER_SEGMENT;
+    const int sched = cfg ? cfg->schedule : DGZ_SCHED_AUTO;
+    const int blocked = sched == DGZ_SCHED_BLOCKED;
+    DGZ_REQUIRE(!dst_pos || variant == DGZ_GATHER_SEGMENT || variant == DGZ_GATHER_BULK,
+                "dgz_gather: destination permutation needs the SEGMENT or BULK variant");
 
     cudaError_t e = cudaSuccess;
     if (variant == DGZ_GATHER_SEGMENT) {
@@ -269,10 +313,11 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n
         if (blocks > need) blocks = need;
         const uint64_t x = (uint64_t)t->row_bytes | ((uint64_t)(uintptr_t)t->dev & 15u) | ((uint64_t)(uintptr_t)out & 15u) | 16u;
         const int sw = (int)(x & (~x + 1));
+        SegLaunch L{dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s};
         if (idx_is64)
-            e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, s);
+            e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, L);
         else
-            e = launch_segment_sw<int32_t>(sw, t, (const int32_t*)idx, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, s);
+            e = launch_segment_sw<int32_t>(sw, t, (const int32_t*)idx, L);
     } else if (variant == DGZ_GATHER_NAIVE || variant == DGZ_GATHER_SHIFT) {
         int64_t blocks = (int64_t)k * 4;
         const bool sh = variant == DGZ_GATHER_SHIFT;
@@ -283,7 +328,7 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n
             e = sh ? launch_elem<true>(t, (const int32_t*)idx, n, n_dev, out, err, (int)blocks, s)
                    : launch_elem<false>(t, (const int32_t*)idx, n, n_dev, out, err, (int)blocks, s);
     } else if (variant == DGZ_GATHER_BULK) {
-        return dgz_gather_bulk(t, idx, idx_is64, n, n_dev, out, err, k, warps, cps, s);
+        return dgz_gather_bulk(t, idx, idx_is64, dst_pos, n, n_dev, out, err, k, warps, blocked, s);
     } else {
         set_error("dgz_gather: unknown variant %d", variant);
         return DGZ_ERR_INVALID;
@@ -293,14 +338,20 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, int64_t n
 }
 
 extern "C" dgz_status dgz_gather(dgz_table t, const int64_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
-    return dgz_gather_impl(t, idx_dev, 1, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 1, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" dgz_status dgz_gather_i32(dgz_table t, const int32_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
-    return dgz_gather_impl(t, idx_dev, 0, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 0, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n, const int64_t* n_dev, void* out_dev,
                                     const dgz_gather_cfg* cfg, dgz_stream stream) {
-    return dgz_gather_impl(t, idx_dev, 1, n, n_dev, out_dev, cfg, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 1, nullptr, n, n_dev, out_dev, cfg, (cudaStream_t)stream);
+}
+
+extern "C" dgz_status dgz_gather_perm(dgz_table t, const int64_t* idx_dev, const int64_t* dst_pos_dev, int64_t n,
+                                      const int64_t* n_dev, void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream) {
+    DGZ_REQUIRE(dst_pos_dev || n == 0, "dgz_gather_perm: null dst_pos");
+    return dgz_gather_impl(t, idx_dev, 1, dst_pos_dev, n, n_dev, out_dev, cfg, (cudaStream_t)stream);
 }

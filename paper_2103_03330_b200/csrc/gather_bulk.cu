@@ -48,9 +48,9 @@ template <> struct piece_t<1> { using T = uint8_t; };
 // smem layout: [full mbarriers x S][empty mbarriers x S][slot metadata x S][pad][S slots]
 template <int SW, typename IdxT>
 __global__ void __launch_bounds__(1024, 1)
-gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx, int64_t n_cap,
-                   const int64_t* __restrict__ n_dev, uint8_t* __restrict__ dst, int* __restrict__ err, int S,
-                   int slot_bytes) {
+gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
+                   const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
+                   uint8_t* __restrict__ dst, int* __restrict__ err, int S, int slot_bytes, int blocked) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
@@ -73,10 +73,19 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // rows of this CTA: r = blockIdx.x + j * gridDim.x, job j uses slot j % S
-    const int64_t first = blockIdx.x;
-    const int64_t stride = gridDim.x;
-    const int64_t njobs = first < n ? (n - 1 - first) / stride + 1 : 0;
+    // rows of this CTA: blocked = the contiguous range [first, first + njobs), else the
+    // row-cyclic set first + j * gridDim.x; job j uses slot j % S
+    int64_t first, stride, njobs;
+    if (blocked) {
+        const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+        first = int64_t(blockIdx.x) * per;
+        stride = 1;
+        njobs = first < n ? min(per, n - first) : 0;
+    } else {
+        first = blockIdx.x;
+        stride = gridDim.x;
+        njobs = first < n ? (n - 1 - first) / stride + 1 : 0;
+    }
     const uint64_t base = reinterpret_cast<uint64_t>(src);
 
     if (warp == 0) {
@@ -111,7 +120,8 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
             const int off = meta[s];
             if (off >= 0) {
                 const uint8_t* sp = slots + (size_t)s * slot_bytes + off;
-                uint8_t* dp = dst + (first + j * stride) * R;
+                const int64_t r = first + j * stride;
+                uint8_t* dp = dst + (dst_pos ? dst_pos[r] : r) * R;
                 for (int64_t q = (int64_t)lane * SW; q < R; q += 32 * SW)
                     *reinterpret_cast<P*>(dp + q) = *reinterpret_cast<const P*>(sp + q);
             }
@@ -122,8 +132,8 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
 }
 
 template <int SW, typename IdxT>
-cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, uint8_t* out, int* err, int blocks,
-                        int threads, cudaStream_t s) {
+cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, const int64_t* dst_pos, int64_t n, const int64_t* n_dev, uint8_t* out,
+                        int* err, int blocks, int threads, int blocked, cudaStream_t s) {
     const int slot_bytes = (int)(((t->row_bytes + 32 + 127) / 128) * 128);
     const int max_smem = 227 * 1024;
     int S = (max_smem - 256) / (slot_bytes + 20);
@@ -132,26 +142,27 @@ cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, int64_t n, const 
     const size_t smem = (((size_t)S * 20 + 127) & ~size_t(127)) + (size_t)S * slot_bytes;
     cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<SW, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    gather_bulk_kernel<SW, IdxT><<<blocks, threads, smem, s>>>(t->dev, t->rows, t->row_bytes, idx, n, n_dev, out, err, S, slot_bytes);
+    gather_bulk_kernel<SW, IdxT><<<blocks, threads, smem, s>>>(t->dev, t->rows, t->row_bytes, idx, dst_pos, n, n_dev, out, err, S,
+                                                               slot_bytes, blocked);
     return cudaGetLastError();
 }
 
 template <typename IdxT>
-cudaError_t launch_bulk_sw(int sw, const dgz_table_s* t, const IdxT* idx, int64_t n, const int64_t* n_dev, uint8_t* out, int* err,
-                           int blocks, int threads, cudaStream_t s) {
+cudaError_t launch_bulk_sw(int sw, const dgz_table_s* t, const IdxT* idx, const int64_t* dst_pos, int64_t n, const int64_t* n_dev,
+                           uint8_t* out, int* err, int blocks, int threads, int blocked, cudaStream_t s) {
     switch (sw) {
-        case 16: return launch_bulk<16>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        case 8: return launch_bulk<8>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        case 4: return launch_bulk<4>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        case 2: return launch_bulk<2>(t, idx, n, n_dev, out, err, blocks, threads, s);
-        default: return launch_bulk<1>(t, idx, n, n_dev, out, err, blocks, threads, s);
+        case 16: return launch_bulk<16>(t, idx, dst_pos, n, n_dev, out, err, blocks, threads, blocked, s);
+        case 8: return launch_bulk<8>(t, idx, dst_pos, n, n_dev, out, err, blocks, threads, blocked, s);
+        case 4: return launch_bulk<4>(t, idx, dst_pos, n, n_dev, out, err, blocks, threads, blocked, s);
+        case 2: return launch_bulk<2>(t, idx, dst_pos, n, n_dev, out, err, blocks, threads, blocked, s);
+        default: return launch_bulk<1>(t, idx, dst_pos, n, n_dev, out, err, blocks, threads, blocked, s);
     }
 }
 
 }  // namespace
 
-dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, int64_t n, const int64_t* n_dev, void* out,
-                           int* err, int sms, int warps, int ctas_per_sm, cudaStream_t s) {
+dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n,
+                           const int64_t* n_dev, void* out, int* err, int sms, int warps, int blocked, cudaStream_t s) {
     using namespace dgz;
     DGZ_REQUIRE(t->row_bytes <= 64 * 1024, "BULK gather: rows above 64 KiB are not supported");
     if (warps < 2) warps = 2;
@@ -159,12 +170,11 @@ dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, 
     // keeps the source's 16 B phase, so the smem read address is SW-aligned as well
     const uint64_t x = (uint64_t)t->row_bytes | ((uint64_t)(uintptr_t)t->dev & 15u) | ((uint64_t)(uintptr_t)out & 15u) | 16u;
     const int sw = (int)(x & (~x + 1));
-    (void)ctas_per_sm;  // one CTA per SM: the ring takes the whole shared memory
     cudaError_t e;
     if (idx_is64)
-        e = launch_bulk_sw<int64_t>(sw, t, (const int64_t*)idx, n, n_dev, (uint8_t*)out, err, sms, warps * 32, s);
+        e = launch_bulk_sw<int64_t>(sw, t, (const int64_t*)idx, dst_pos, n, n_dev, (uint8_t*)out, err, sms, warps * 32, blocked, s);
     else
-        e = launch_bulk_sw<int32_t>(sw, t, (const int32_t*)idx, n, n_dev, (uint8_t*)out, err, sms, warps * 32, s);
+        e = launch_bulk_sw<int32_t>(sw, t, (const int32_t*)idx, dst_pos, n, n_dev, (uint8_t*)out, err, sms, warps * 32, blocked, s);
     if (e != cudaSuccess) return cuda_fail(e, "bulk gather launch");
     return DGZ_OK;
 }

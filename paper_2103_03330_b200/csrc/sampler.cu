@@ -167,6 +167,53 @@ bitmap_emit_kernel(uint32_t* __restrict__ front, uint32_t* __restrict__ cand, co
     }
 }
 
+// ---- U in ascending order (the final frontier bitmap) with each ID's position in U ----------
+__global__ void __launch_bounds__(kChunkThreads)
+bitmap_count_all_kernel(const uint32_t* __restrict__ front, int64_t* __restrict__ chunk_sums) {
+    using BR = cub::BlockReduce<int, kChunkThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t w0 = int64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
+    const uint4* cf = reinterpret_cast<const uint4*>(front + w0);
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread / 4; ++q) {
+        const uint4 b = cf[q];
+        c += __popc(b.x) + __popc(b.y) + __popc(b.z) + __popc(b.w);
+    }
+    const int tot = BR(tmp).Sum(c);
+    if (threadIdx.x == 0) chunk_sums[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(kChunkThreads)
+bitmap_emit_sorted_kernel(const uint32_t* __restrict__ front, const int64_t* __restrict__ chunk_offs, const int32_t* __restrict__ pos,
+                          int64_t* __restrict__ sorted, int64_t* __restrict__ sorted_pos) {
+    using BS = cub::BlockScan<int, kChunkThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t w0 = int64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
+    uint32_t w[kWordsPerThread];
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        w[q] = front[w0 + q];
+        c += __popc(w[q]);
+    }
+    int ex;
+    BS(tmp).ExclusiveSum(c, ex);
+    if (!c) return;
+    int64_t p = chunk_offs[blockIdx.x] + ex;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        uint32_t bits = w[q];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            const int64_t id = (w0 + q) * 32 + b;
+            sorted[p] = id;
+            sorted_pos[p] = pos[id];
+            ++p;
+            bits &= bits - 1;
+        }
+    }
+}
+
 // ---- seeds: F_0 = seeds with the first occurrence of each ID kept -----------------------------
 __global__ void seeds_mark_kernel(const int64_t* __restrict__ seeds, int64_t n, int64_t N, int32_t* __restrict__ pos, int* err) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -249,7 +296,7 @@ Layout layout(int64_t N, int64_t max_seeds) {
     l.o_err = o; o = al(o + 8);  // first: dgz_sample_check finds it without the layout
     l.o_front = o; o = al(o + 4 * (size_t)l.nwords_pad);
     l.o_cand = o; o = al(o + 4 * (size_t)l.nwords_pad);
-    l.o_csum = o; o = al(o + 8 * (size_t)l.nchunks);
+    l.o_csum = o; o = al(o + 8 * ((size_t)l.nchunks + 1));
     l.o_coff = o; o = al(o + 8 * (size_t)l.nchunks);
     l.o_ssum = o; o = al(o + 8 * (size_t)l.seed_chunks);
     l.o_soff = o; o = al(o + 8 * (size_t)l.seed_chunks);
@@ -317,6 +364,7 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
                 (long long)be);
     DGZ_REQUIRE(!out->nbr_local || (out->nbr && out->blocks_cap >= be), "dgz_sample_uniform: nbr_local needs nbr");
     DGZ_REQUIRE(!out->cnt || out->cnt_cap >= ce, "dgz_sample_uniform: cnt capacity");
+    DGZ_REQUIRE(!out->ids_sorted == !out->ids_sorted_pos, "dgz_sample_uniform: ids_sorted and ids_sorted_pos go together");
     const Layout l = layout(N, n_seeds);
     DGZ_REQUIRE(out->workspace && out->workspace_bytes >= l.total, "dgz_sample_uniform: workspace %zu < %zu bytes",
                 out->workspace_bytes, l.total);
@@ -366,8 +414,14 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
         nbr_off += bounds[k] * f;
         cnt_off += bounds[k];
     }
+    if (out->nbr_local || out->ids_sorted) posmap_kernel<<<grid_for(bounds[n_layers], 256), 256, 0, s>>>(out->ids, sizes, n_layers, pos);
+    if (out->ids_sorted) {
+        // the final frontier bitmap holds exactly U: compact it in ascending ID order
+        bitmap_count_all_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, csum);
+        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, nullptr, csum + l.nchunks);
+        bitmap_emit_sorted_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, coff, pos, out->ids_sorted, out->ids_sorted_pos);
+    }
     if (out->nbr_local) {
-        posmap_kernel<<<grid_for(bounds[n_layers], 256), 256, 0, s>>>(out->ids, sizes, n_layers, pos);
         int64_t o = 0;
         for (int k = 0; k < n_layers; ++k) {
             if (fanouts[k] > 0)

@@ -23,9 +23,10 @@ _lib = ctypes.CDLL(_SO)
 # --- constants (dgz.h) -------------------------------------------------------------------------
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_RANGE, ERR_STATE = range(6)
 F32, F16, BF16, U8 = range(4)
-REG_PORTABLE, REG_READONLY, REG_NO_PIN = 1, 2, 4
-HOST_HUGEPAGE, HOST_POPULATE = 1, 2
+REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED = 1, 2, 4, 8
+HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM = 1, 2, 4
 GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
+SCHED_AUTO, SCHED_INTERLEAVED, SCHED_BLOCKED = range(3)
 MAX_FANOUT, MAX_LAYERS = 64, 8
 ELEM_BYTES = {F32: 4, F16: 2, BF16: 2, U8: 1}
 TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16, U8: torch.uint8}
@@ -57,8 +58,8 @@ class TableInfo(ctypes.Structure):
 
 
 class GatherCfg(ctypes.Structure):
-    _fields_ = [("variant", ctypes.c_int32), ("sm_count", ctypes.c_int32),
-                ("warps_per_cta", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32)]
+    _fields_ = [("variant", ctypes.c_int32), ("sm_count", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
+                ("ctas_per_sm", ctypes.c_int32), ("schedule", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class Csr(ctypes.Structure):
@@ -70,7 +71,8 @@ class SampleOut(ctypes.Structure):
     _fields_ = [("ids", ctypes.c_void_p), ("ids_cap", ctypes.c_int64), ("sizes_dev", ctypes.c_void_p),
                 ("sizes_host", ctypes.c_void_p), ("nbr", ctypes.c_void_p), ("nbr_local", ctypes.c_void_p),
                 ("cnt", ctypes.c_void_p), ("blocks_cap", ctypes.c_int64), ("cnt_cap", ctypes.c_int64),
-                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("ids_sorted", ctypes.c_void_p), ("ids_sorted_pos", ctypes.c_void_p)]
 
 
 _vp, _i64, _i32, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
@@ -84,12 +86,15 @@ _SIGS = {
     "dgz_host_alloc": ([ctypes.c_char_p, _sz, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
     "dgz_host_free": ([_vp, _sz], ctypes.c_int),
     "dgz_host_unlink": ([ctypes.c_char_p], ctypes.c_int),
+    "dgz_host_export": ([_vp, _P(ctypes.c_int)], ctypes.c_int),
+    "dgz_host_import": ([ctypes.c_int, _sz, _P(_vp)], ctypes.c_int),
     "dgz_register_table": ([_vp, _i64, _i64, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
     "dgz_unregister_table": ([_vp], ctypes.c_int),
     "dgz_table_get_info": ([_vp, _P(TableInfo)], ctypes.c_int),
     "dgz_gather": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_gather_i32": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_gather_ex": ([_vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
+    "dgz_gather_perm": ([_vp, _vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
     "dgz_check_errors": ([_vp, _vp], ctypes.c_int),
     "dgz_sample_bounds": ([_i64, _i64, _P(_i32), ctypes.c_int, _P(_i64), _P(_i64), _P(_i64)], ctypes.c_int),
     "dgz_sample_workspace_bytes": ([_i64, _i64, _P(_sz)], ctypes.c_int),
@@ -139,13 +144,22 @@ def _dptr(t: torch.Tensor | None) -> int | None:
 class HostBuffer:
     """Host mapping from dgz_host_alloc (anonymous or /dev/shm shared)."""
 
-    def __init__(self, nbytes: int, shm_name: str | None = None, create: bool = True, flags: int = HOST_HUGEPAGE):
+    def __init__(self, nbytes: int, shm_name: str | None = None, create: bool = True, flags: int = HOST_HUGEPAGE,
+                 import_fd: int | None = None):
         p = _vp()
-        name = shm_name.encode() if shm_name else None
-        _check(_lib.dgz_host_alloc(name, nbytes, int(create), flags, ctypes.byref(p)), "dgz_host_alloc")
+        if import_fd is not None:
+            _check(_lib.dgz_host_import(import_fd, nbytes, ctypes.byref(p)), "dgz_host_import")
+        else:
+            name = shm_name.encode() if shm_name else None
+            _check(_lib.dgz_host_alloc(name, nbytes, int(create), flags, ctypes.byref(p)), "dgz_host_alloc")
         self.ptr = p.value
         self.nbytes = nbytes
         self.shm_name = shm_name
+
+    def export_fd(self) -> int:
+        fd = ctypes.c_int(-1)
+        _check(_lib.dgz_host_export(self.ptr, ctypes.byref(fd)), "dgz_host_export")
+        return fd.value
 
     def numpy(self, offset: int = 0, nbytes: int | None = None):
         import numpy as np
@@ -212,8 +226,9 @@ def unregister_table(t: Table) -> None:
 
 
 # --- gather ------------------------------------------------------------------------------------
-def gather_cfg(variant: int = GATHER_AUTO, sm_count: int = 0, warps_per_cta: int = 0, ctas_per_sm: int = 0) -> GatherCfg:
-    return GatherCfg(variant, sm_count, warps_per_cta, ctas_per_sm)
+def gather_cfg(variant: int = GATHER_AUTO, sm_count: int = 0, warps_per_cta: int = 0, ctas_per_sm: int = 0,
+               schedule: int = SCHED_AUTO) -> GatherCfg:
+    return GatherCfg(variant, sm_count, warps_per_cta, ctas_per_sm, schedule, 0)
 
 
 def gather(table: Table, idx: torch.Tensor, out: torch.Tensor, n: int | None = None, n_dev: torch.Tensor | None = None,
@@ -231,6 +246,17 @@ def gather(table: Table, idx: torch.Tensor, out: torch.Tensor, n: int | None = N
     else:
         _check(_lib.dgz_gather_ex(table.handle, _dptr(idx), n, _dptr(n_dev), _dptr(out),
                                   ctypes.byref(cfg) if cfg is not None else None, s), "dgz_gather_ex")
+    return out
+
+
+def gather_perm(table: Table, idx: torch.Tensor, dst_pos: torch.Tensor, out: torch.Tensor, n: int | None = None,
+                n_dev: torch.Tensor | None = None, cfg: GatherCfg | None = None, stream=None) -> torch.Tensor:
+    """out[dst_pos[k]] = table[idx[k]] (dgz_gather_perm): fetch in table order, scatter to HBM."""
+    n = idx.numel() if n is None else n
+    assert idx.dtype == torch.int64 and dst_pos.dtype == torch.int64
+    assert out.numel() * out.element_size() >= n * table.row_bytes, "out too small"
+    _check(_lib.dgz_gather_perm(table.handle, _dptr(idx), _dptr(dst_pos), n, _dptr(n_dev), _dptr(out),
+                                ctypes.byref(cfg) if cfg is not None else None, _stream(stream)), "dgz_gather_perm")
     return out
 
 
@@ -261,7 +287,8 @@ def sample_workspace_bytes(n_nodes: int, max_seeds: int) -> int:
 class SampleBuffers:
     """Caller-owned outputs + workspace of dgz_sample_uniform, sized by dgz_sample_bounds."""
 
-    def __init__(self, n_nodes: int, max_seeds: int, fanouts, device=None, blocks: bool = True, local: bool = True):
+    def __init__(self, n_nodes: int, max_seeds: int, fanouts, device=None, blocks: bool = True, local: bool = True,
+                 sorted_ids: bool = True):
         device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.fanouts = tuple(int(f) for f in fanouts)
         self.bounds, be, ce = sample_bounds(n_nodes, max_seeds, self.fanouts)
@@ -272,11 +299,13 @@ class SampleBuffers:
         self.nbr = torch.empty(max(be, 1), dtype=torch.int64, device=device) if blocks else None
         self.cnt = torch.empty(max(ce, 1), dtype=torch.int32, device=device) if blocks else None
         self.local = torch.empty(max(be, 1), dtype=torch.int32, device=device) if (blocks and local) else None
+        self.ids_sorted = torch.empty_like(self.ids) if sorted_ids else None
+        self.ids_sorted_pos = torch.empty_like(self.ids) if sorted_ids else None
         wsb = sample_workspace_bytes(n_nodes, max_seeds)
         self.workspace = torch.empty(wsb, dtype=torch.uint8, device=device)
         self.struct = SampleOut(self.ids.data_ptr(), self.ids.numel(), self.sizes_dev.data_ptr(), self.sizes_host.data_ptr(),
                                 _dptr(self.nbr), _dptr(self.local), _dptr(self.cnt), be, ce,
-                                self.workspace.data_ptr(), wsb)
+                                self.workspace.data_ptr(), wsb, _dptr(self.ids_sorted), _dptr(self.ids_sorted_pos))
 
     def hop_blocks(self, sizes=None):
         """Per-hop (nbr [n_k x f_k], cnt [n_k], local [n_k x f_k]) views (after a sync)."""

@@ -192,6 +192,10 @@ def _compare_plan(off, col, seeds, fanouts, rng_seed, col64=False):
     assert sizes == want.sizes.tolist()
     assert bufs.sizes_dev.cpu().tolist() == sizes
     assert np.array_equal(bufs.ids[:sizes[-1]].cpu().numpy(), want.U)
+    n = sizes[-1]
+    srt = bufs.ids_sorted[:n].cpu().numpy()
+    assert np.array_equal(srt, np.sort(want.U))
+    assert np.array_equal(want.U[bufs.ids_sorted_pos[:n].cpu().numpy()], srt)
     for k, (nbr, cnt, loc) in enumerate(bufs.hop_blocks()):
         assert np.array_equal(cnt.cpu().numpy(), want.cnt[k])
         assert np.array_equal(nbr.cpu().numpy(), want.nbr[k])
@@ -256,5 +260,52 @@ def test_sample_then_gather_device_count(dev):
         n = want.U.shape[0]
         exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
         assert np.array_equal(out[:n * c.row_bytes].cpu().numpy().reshape(n, -1), exp)
+    finally:
+        t.close()
+
+
+@pytest.mark.parametrize("variant", [1, 4])
+@pytest.mark.parametrize("sched", [0, 1, 2])
+@pytest.mark.parametrize("R,base", [(512, 0), (400, 16), (2408, 8), (100, 4), (20, 0)])
+def test_gather_perm(dev, variant, sched, R, base):
+    rows = 4000
+    t = HostTable(rows, R, seed=R + 99, base=base, dtype=dgz.F32)
+    try:
+        idx = gen.random_ids(rows, 1500 + 7, seed=R)
+        want, _ = oracle.gather(t.np, R, idx)
+        order = np.argsort(idx, kind="stable")
+        ids_s = torch.from_numpy(idx[order]).cuda()
+        pos_s = torch.from_numpy(order.astype(np.int64)).cuda()
+        out = torch.full((idx.shape[0] * R,), 0xAB, dtype=torch.uint8, device="cuda")
+        for sms in (0, 3, 64):
+            out.fill_(0xAB)
+            dgz.gather_perm(t.table, ids_s, pos_s, out, cfg=dgz.gather_cfg(variant=variant, schedule=sched, sm_count=sms))
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy().reshape(-1, R), want), sms
+    finally:
+        t.close()
+
+
+@pytest.mark.parametrize("cid", [1, 3])
+def test_step_sorted_gather_matches_oracle(dev, cid):
+    """The bench step: GPU sampler (sorted outputs) -> dgz_gather_perm with the device count."""
+    c = gen.CONFIGS[cid]
+    n_nodes = c.n_nodes
+    off, col = gen.gen_csr(n_nodes, c.avg_degree, c.seed)
+    t = HostTable(n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        for j in (0, 5):
+            seeds = gen.batch_seeds(n_nodes, c.batch, c.seed, j)
+            rs = gen.batch_rng_seed(c.seed, j)
+            g, bufs = _sample_dev(off, col, seeds, c.fanouts, rs)
+            L = len(c.fanouts)
+            out = torch.empty(bufs.bounds[-1] * c.row_bytes, dtype=torch.uint8, device="cuda")
+            dgz.gather_perm(t.table, bufs.ids_sorted, bufs.ids_sorted_pos, out, n=bufs.bounds[-1],
+                            n_dev=bufs.sizes_dev[L:L + 1])
+            torch.cuda.synchronize()
+            want = oracle.sample_uniform(off, col, seeds, c.fanouts, rs, with_blocks=False)
+            n = want.U.shape[0]
+            exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+            assert np.array_equal(out[:n * c.row_bytes].cpu().numpy().reshape(n, -1), exp)
     finally:
         t.close()
