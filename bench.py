@@ -1,0 +1,611 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path of arXiv 2103.03330 on B200: GPU sampling + zero-copy feature gather.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (one process per GPU)
+
+A step = one minibatch fetch: seeds of global batch j (j = i*G + rank)
+-> dgz_sample_uniform (3-hop uniform sampling on the GPU, CSR in HBM) -> dgz_gather_perm
+(rows of the pinned, mapped host table read by zero-copy over PCIe into HBM).  Metric:
+gathered feature GB/s (useful bytes n*R / time, GB = 1e9), whole-job aggregate over ranks.
+Inputs are resident (CSR and per-step seeds in HBM, table pinned) before the timed region;
+the 56.9 GB table and fresh minibatches every step are far larger than the 126 MB L2.
+
+Rank 0 prints ONE JSON line.  ``--impl reference`` times the CPU oracle (oracle/, a plain
+single-threaded C sampler + row gather) on the same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+import dgz_inputs as gen  # noqa: E402
+
+METRIC = "gathered feature GB/s per GPU and aggregate at 1/2/4/8 B200 vs PCIe Gen5 roofline"
+UNIT = "GB/s"
+
+
+# ----------------------------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------------------------
+class Dist:
+    def __init__(self, want_gpus: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if torch.cuda.is_available():
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.pg = dist
+        elif torch.cuda.is_available():
+            torch.cuda.set_device(0)
+        if want_gpus != self.world and self.rank == 0:
+            print(f"# note: --gpus {want_gpus} but WORLD_SIZE {self.world}; using {self.world}", file=sys.stderr)
+
+    def barrier(self):
+        if self.pg:
+            if torch.cuda.is_available():
+                self.pg.barrier(device_ids=[self.local])
+            else:
+                self.pg.barrier()
+
+    def allreduce(self, vals, op="sum"):
+        if not self.pg:
+            return list(vals)
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM if op == "sum" else self.pg.ReduceOp.MAX)
+        return t.cpu().tolist()
+
+    def bcast_obj(self, obj):
+        if not self.pg:
+            return obj
+        lst = [obj]
+        self.pg.broadcast_object_list(lst, src=0)
+        return lst[0]
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+# ----------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[3]) for r in self.rows if len(r) > 8 and r[3].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+# ----------------------------------------------------------------------------------------------
+# shared inputs
+# ----------------------------------------------------------------------------------------------
+def make_table(cfg, d: Dist, dgz):
+    """Host feature table: one copy on the box, registered by every rank."""
+    nbytes = cfg.table_bytes
+    if d.world == 1:
+        buf = dgz.HostBuffer(nbytes + 4096, flags=dgz.HOST_HUGEPAGE)
+        t0 = time.time()
+        gen.fill_table(buf.ptr, nbytes, cfg.seed)
+        fill_s = time.time() - t0
+    else:
+        name = f"/dgz_bench_c{cfg.cid}_{os.environ.get('MASTER_PORT', '0')}"
+        fill_s = 0.0
+        if d.rank == 0:
+            buf = dgz.HostBuffer(nbytes + 4096, shm_name=name, create=True, flags=dgz.HOST_HUGEPAGE)
+            t0 = time.time()
+            gen.fill_table(buf.ptr, nbytes, cfg.seed)
+            fill_s = time.time() - t0
+        d.barrier()
+        if d.rank != 0:
+            buf = dgz.HostBuffer(nbytes + 4096, shm_name=name, create=False, flags=dgz.HOST_HUGEPAGE)
+        d.barrier()
+        if d.rank == 0:
+            buf.unlink()   # the mappings stay valid; the name does not outlive the run
+    return buf, fill_s
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def measure_ceilings(dgz, table_info, R):
+    """In-run PCIe ceilings: H2D DMA from pinned memory, zero-copy streaming read, RTT."""
+    h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        dbuf.copy_(h, non_blocking=True)
+    a, b = ev(), ev()
+    trials = []
+    for _ in range(5):  # best of 5 x (10 copies of 256 MiB)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(10):
+            dbuf.copy_(h, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        trials.append(10 * (256 << 20) / (a.elapsed_time(b) * 1e-3) / 1e9)
+    dma = max(trials)
+    del h
+    sink = torch.zeros(2, dtype=torch.int64, device="cuda")
+    zbytes = 1 << 30
+    pbuf = dgz.HostBuffer(zbytes, flags=dgz.HOST_HUGEPAGE)
+    pbuf.numpy()[::4096] = 1
+    ptab = dgz.register_table(pbuf.ptr, zbytes // 128, 128, dgz.U8)
+    dgz.probe_stream(ptab.info.dev_ptr, zbytes, 8, 32, 8, sink)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(4):
+        dgz.probe_stream(ptab.info.dev_ptr, zbytes, 8, 32, 8, sink)
+    b.record()
+    torch.cuda.synchronize()
+    zc = 4 * zbytes / (a.elapsed_time(b) * 1e-3) / 1e9
+    ptab.unregister()
+    pbuf.free()
+    del dbuf
+    return {"h2d_dma_gbs": round(dma, 2), "h2d_dma_trials": [round(x, 2) for x in trials], "zc_stream_gbs": round(zc, 2),
+            "how": "best of 5 x (cudaMemcpyAsync 256 MiB pinned H2D x10); zero-copy LDG.128 stream over a 1 GiB pinned buffer x4 on 8 SMs"}
+
+
+def load_profile_traffic(cid):
+    """dram bytes per gather launch from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_gather_summary.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        c = j.get(f"config{cid}")
+        return c if c else None
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------------
+# our implementation
+# ----------------------------------------------------------------------------------------------
+def run_ours(args, d: Dist):
+    from paper_2103_03330_b200 import dgz
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+
+    cfg = gen.CONFIGS[args.config]
+    R = cfg.row_bytes
+    L = len(cfg.fanouts)
+    t_setup = time.time()
+    buf, fill_s = make_table(cfg, d, dgz)
+    table = dgz.register_table(buf.ptr, cfg.n_nodes, cfg.dim, dgz.F32)
+    info = table.info
+    t0 = time.time()
+    off, col = gen.gen_csr(cfg.n_nodes, cfg.avg_degree, cfg.seed)
+    csr_s = time.time() - t0
+    graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+    n_edges = int(off[-1])
+    del off, col
+
+    K, W = args.steps, args.warmup
+    G, rank = d.world, d.rank
+    batches = [i * G + rank for i in range(W + K)]
+    seeds_host = [torch.from_numpy(gen.batch_seeds(cfg.n_nodes, cfg.batch, cfg.seed, j)) for j in batches]
+    seeds_dev = [x.cuda() for x in seeds_host]
+    rng = [gen.batch_rng_seed(cfg.seed, j) for j in batches]
+
+    gcfg = dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps)
+    fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True)
+    cap = fetcher.bufs[0].bounds[-1]
+    n_steps = torch.zeros(W + K, dtype=torch.int64, device="cuda")
+    s = fetcher.stream
+    ceilings = measure_ceilings(dgz, info, R)
+    # per-step events on the fetch stream (torch.cuda.Event only sees the stream it is recorded on)
+    e_s = [ev() for _ in range(W + K)]
+    e_g = [ev() for _ in range(W + K)]
+    e_e = [ev() for _ in range(W + K)]
+
+    def step(i):
+        p = i % 2
+        b = fetcher.bufs[p]
+        e_s[i].record(s)
+        with torch.cuda.stream(s):
+            dgz.sample_uniform(graph, seeds_dev[i], cfg.fanouts, rng[i], b, stream=s)
+            e_g[i].record(s)
+            dgz.gather_perm(table, b.ids_sorted, b.ids_sorted_pos, fetcher.rows[p], n=cap, n_dev=b.sizes_dev[L:L + 1],
+                            cfg=gcfg, stream=s)
+            e_e[i].record(s)
+            n_steps[i:i + 1].copy_(b.sizes_dev[L:L + 1], non_blocking=True)
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    d.barrier()
+    torch.cuda.synchronize()
+    launches0 = dgz.kernel_launches()
+    t_start, t_end = ev(), ev()
+    with ClockSampler(d.local) as clk:
+        t_start.record(s)
+        for i in range(W, W + K):
+            step(i)
+        t_end.record(s)
+        torch.cuda.synchronize()
+    launches = dgz.kernel_launches() - launches0
+    d.barrier()
+    torch.cuda.synchronize()
+    dgz.check_errors(table)
+    elapsed = t_start.elapsed_time(t_end) * 1e-3
+    ns = n_steps.cpu().tolist()[W:]
+    bytes_rank = float(sum(ns) * R)
+    gather_ms = [e_g[i].elapsed_time(e_e[i]) for i in range(W, W + K)]
+    sample_ms = [e_s[i].elapsed_time(e_g[i]) for i in range(W, W + K)]
+    step_ms = [e_s[i].elapsed_time(e_e[i]) for i in range(W, W + K)]
+    tot_bytes, = d.allreduce([bytes_rank], "sum")
+    max_el, = d.allreduce([elapsed], "max")
+    value = tot_bytes / max_el / 1e9
+    per_gpu = bytes_rank / elapsed / 1e9
+    gather_gbs = float(np.mean(ns)) * R / (float(np.mean(gather_ms)) * 1e-3) / 1e9
+
+    # keep the last two minibatches for the oracle parity check (cpu_baseline leg)
+    last = {}
+    for i in (W + K - 2, W + K - 1):
+        p = i % 2
+        n = ns[i - W]
+        last[batches[i]] = (fetcher.bufs[p].ids[:n].cpu().numpy(), fetcher.rows[p][:n].cpu().numpy(), rng[i],
+                            seeds_host[i].numpy())
+
+    # ---- end-to-end through the public API: pinned host seeds -> H2D -> sample -> gather -> D2H |U|
+    e2e = run_e2e(fetcher, cfg, seeds_host, rng, W, K, d)
+
+    # ---- overlap with a stand-in consumer (steps a5-a7)
+    overlap = run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K) if (args.overlap and rank == 0) else None
+
+    # ---- baselines (rank 0 only, N=1 at most the box's cores): oracle + CPU-gather+memcpy
+    cpu_base = dma_base = parity = None
+    if rank == 0 and not args.no_baselines:
+        cpu_base, parity = run_oracle_leg(cfg, buf.ptr, graph, last, d)
+        dma_base = run_dma_baseline(cfg, buf, fetcher, graph, seeds_dev, rng, W, K, d)
+
+    clocks = clk.summary()
+    sm_count = torch.cuda.get_device_properties(0).multi_processor_count
+    traffic = load_profile_traffic(cfg.cid)
+    peak = ceilings["h2d_dma_gbs"]
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": G, "steps": K, "warmup": W,
+        "ms_per_step": round(max_el / K * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 (fp32 rows moved as bytes)", "data": "synthetic",
+        "config": {"workload": f"config{cfg.cid} {cfg.name}: {cfg.n_nodes} nodes, {n_edges} edges "
+                               f"(Poisson avg deg {cfg.avg_degree}), {cfg.dim}x fp32 = {R} B rows, "
+                               f"{cfg.table_bytes / 1e9:.1f} GB pinned host table, fanouts {list(cfg.fanouts)}, "
+                               f"{cfg.batch} seeds per GPU per step",
+                   "global_batch": cfg.batch * G, "parallelism": f"dp{G} (seed partition j mod G)",
+                   "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
+                   "gather": {"variant": "segment", "sm_count": args.gather_sms or 96,
+                              "warps_per_cta": args.gather_warps or 2, "order": "address-sorted + inverse permutation"}},
+        "per_gpu_gbs": round(per_gpu, 3),
+        "roofline": {"bound": "pcie", "achieved": round(gather_gbs, 3), "peak": peak, "unit": "GB/s",
+                     "frac": round(gather_gbs / peak, 4), "traffic": traffic,
+                     "kernel": "gather_segment_kernel (dgz_gather_perm)",
+                     "peak_source": "measured in this run: cudaMemcpyAsync H2D from pinned memory (PCIe Gen5 x16); "
+                                    "MEASURED_PEAKS.json has no PCIe figure",
+                     "algorithmic_bytes_per_launch": round(float(np.mean(ns)) * R),
+                     "gather_ms_mean": round(float(np.mean(gather_ms)), 4),
+                     "zc_stream_frac": round(gather_gbs / ceilings["zc_stream_gbs"], 4),
+                     "hbm_write_frac": round(gather_gbs / 6537.3, 5)},
+        "ceilings": ceilings,
+        "latency_ms": {"step_p10": pct(step_ms, 10), "step_p50": pct(step_ms, 50), "step_p90": pct(step_ms, 90),
+                       "sample_p50": pct(sample_ms, 50), "gather_p50": pct(gather_ms, 50)},
+        "rows_per_step_mean": round(float(np.mean(ns)), 1),
+        "cpu_baseline": cpu_base, "dma_baseline": dma_base, "parity": parity,
+        "e2e": e2e, "overlap": overlap,
+        "gpu_launches": int(launches), "gpu_launches_per_step": round(launches / K, 2),
+        "clocks": clocks,
+        "setup": {"table_fill_s": round(fill_s, 2), "register_s": round(info.register_seconds, 2),
+                  "gpu_mem_mapping_bytes": info.gpu_mem_delta,
+                  "mapping_ratio": round(cfg.table_bytes / max(info.gpu_mem_delta, 1), 1),
+                  "csr_gen_s": round(csr_s, 2), "total_s": round(time.time() - t_setup, 1), "sms": sm_count},
+    }
+    table.unregister()
+    buf.free()
+    return line
+
+
+def pct(xs, q):
+    return round(float(np.percentile(xs, q)), 4)
+
+
+def run_e2e(fetcher, cfg, seeds_host, rng, W, K, d: Dist):
+    """Same metric through the public API with host-resident inputs: per step the seeds go
+    H2D from pinned memory, the fetch runs, and |U| comes back D2H (read on the host)."""
+    R = cfg.row_bytes
+    pinned = [x.pin_memory() for x in seeds_host]
+    total = 0
+
+    def one(i):
+        mb = fetcher.fetch(pinned[i], rng[i])
+        return mb.sizes()[-1]
+    for i in range(W):
+        one(i)
+    torch.cuda.synchronize()
+    d.barrier()
+    t0 = time.perf_counter()
+    for i in range(W, W + K):
+        total += one(i)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    tot, = d.allreduce([float(total * R)], "sum")
+    mx, = d.allreduce([el], "max")
+    L = len(cfg.fanouts)
+    return {"value": round(tot / mx / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": cfg.batch * 8,
+            "d2h_bytes_per_step": (L + 1) * 8, "ms_per_step": round(mx / K * 1e3, 4),
+            "how": "MinibatchFetcher.fetch(pinned host seeds) + host read of |U| every step, wall clock"}
+
+
+def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
+    """Exposed fetch time with a stand-in GraphSAGE mean-aggregation consumer (a5-a7), and the
+    gather-SM sweep (a6: the B200 analogue of the paper's MPS ratio sweep, fig:mps_bandwidth)."""
+    dim = cfg.dim
+    L = len(cfg.fanouts)
+    comp = torch.cuda.Stream()
+    y = torch.empty((fetcher.bufs[0].bounds[L - 1], dim), dtype=torch.float32, device="cuda")
+    nstep = min(K, 10)
+    nb = sum(fetcher.bufs[0].bounds[k] * cfg.fanouts[k] for k in range(L - 1))
+    cb = sum(fetcher.bufs[0].bounds[k] for k in range(L - 1))
+    a, b = ev(), ev()
+    saved = fetcher.cfg
+
+    def consume(mb, repeat):
+        dgz.aggregate_mean(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:], cfg.fanouts[L - 1],
+                           mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], y, repeat=repeat, sm_count=0, stream=comp)
+
+    def fetch_alone():
+        for i in range(2):
+            fetcher.fetch(seeds_dev[i], rng[i])
+        torch.cuda.synchronize()
+        a.record(fetcher.stream)
+        for i in range(nstep):
+            fetcher.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)])
+        b.record(fetcher.stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / nstep
+
+    def consumer_alone(mb, repeat):
+        with torch.cuda.stream(comp):
+            a.record(comp)
+            for _ in range(nstep):
+                consume(mb, repeat)
+            b.record(comp)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / nstep
+
+    def pipelined(repeat):
+        torch.cuda.synchronize()
+        mbs = [fetcher.fetch(seeds_dev[0], rng[0])]
+        start, end = ev(), ev()
+        start.record(comp)
+        for i in range(1, nstep + 1):
+            nxt = fetcher.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)])
+            cur = mbs[-1]
+            comp.wait_event(cur.event)
+            with torch.cuda.stream(comp):
+                consume(cur, repeat)
+            fetcher.release(cur, comp)
+            mbs.append(nxt)
+        comp.wait_event(mbs[-1].event)
+        end.record(comp)
+        torch.cuda.synchronize()
+        return start.elapsed_time(end) / nstep
+
+    # calibrate the consumer to T_c ~ T_g of the default gather
+    fetcher.cfg = dgz.gather_cfg()
+    t_g0 = fetch_alone()
+    mb = fetcher.fetch(seeds_dev[0], rng[0])
+    mb.event.synchronize()
+    repeat = 8
+    for _ in range(3):
+        t_c = consumer_alone(mb, repeat)
+        repeat = max(1, int(round(repeat * t_g0 / t_c)))
+    t_c = consumer_alone(mb, repeat)
+    sweep = []
+    for sms, warps in ((8, 4), (16, 4), (24, 2), (48, 2), (96, 2), (148, 2)):
+        fetcher.cfg = dgz.gather_cfg(sm_count=sms, warps_per_cta=warps)
+        t_g = fetch_alone()
+        t_o = pipelined(repeat)
+        sweep.append({"gather_sms": sms, "warps": warps, "t_fetch_ms": round(t_g, 3), "t_step_overlapped_ms": round(t_o, 3),
+                      "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
+                      "fetch_gbs_alone": round(float(fetcher.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2)})
+    fetcher.cfg = saved
+    best = min(sweep, key=lambda r: r["t_step_overlapped_ms"])
+    return {"t_fetch_ms": round(t_g0, 3), "t_consumer_ms": round(t_c, 3), "consumer_repeat": repeat,
+            "serial_ms": round(t_g0 + t_c, 3), "best": best,
+            "hidden_frac": round(1 - best["exposed_fetch_ms"] / best["t_fetch_ms"], 3), "sm_sweep": sweep,
+            "consumer": "dgz_aggregate_mean over the last hop's block (7 CTAs x 256 thr per SM), repeated to T_c ~ T_g"}
+
+
+def run_oracle_leg(cfg, table_addr, graph, last, d: Dist):
+    """cpu_baseline: the oracle as it stands (single-threaded C) on a bounded sample of the
+    same workload, plus a full-size exact parity check of the GPU's last two minibatches."""
+    import oracle
+    off = graph.offsets.cpu().numpy()
+    col = graph.cols.cpu().numpy()
+    R = cfg.row_bytes
+    parity = {"batches": [], "exact": True}
+    t_total, bytes_total, nb = 0.0, 0, 0
+    budget = 20.0
+    for j, (U_gpu, rows_gpu, rs, seeds) in last.items():
+        t0 = time.perf_counter()
+        s, outb = oracle.sample_and_gather(off, col, seeds, cfg.fanouts, rs, table_addr, cfg.n_nodes, R)
+        t_total += time.perf_counter() - t0
+        n = s.U.shape[0]
+        bytes_total += n * R
+        nb += 1
+        ok_u = bool(np.array_equal(s.U, U_gpu))
+        ok_rows = ok_u and bool(np.array_equal(outb[:n * R].reshape(n, R), rows_gpu))
+        parity["batches"].append({"j": int(j), "rows": int(n), "ids_equal": ok_u, "rows_equal": ok_rows})
+        parity["exact"] &= ok_u and ok_rows
+    # more minibatches (not compared) until ~budget seconds of oracle work
+    j = 10_000_000
+    while t_total < budget and nb < 40:
+        seeds = gen.batch_seeds(cfg.n_nodes, cfg.batch, cfg.seed, j)
+        rs = gen.batch_rng_seed(cfg.seed, j)
+        t0 = time.perf_counter()
+        s, _ = oracle.sample_and_gather(off, col, seeds, cfg.fanouts, rs, table_addr, cfg.n_nodes, R)
+        t_total += time.perf_counter() - t0
+        bytes_total += s.U.shape[0] * R
+        nb += 1
+        j += 1
+    return ({"value": round(bytes_total / t_total / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+             "sample": f"{nb} config{cfg.cid} minibatches (sample + gather, {t_total:.1f} s single-threaded C)",
+             "s_per_minibatch": round(t_total / nb, 3), "host_cores": os.cpu_count()}, parity)
+
+
+def run_dma_baseline(cfg, buf, fetcher, graph, seeds_dev, rng, W, K, d: Dist):
+    """The paper's DMA-based method: CPU gathers the sampled rows into a pinned
+    staging buffer with T threads, then cudaMemcpyAsync H2D; double-buffered so the CPU gather
+    of j+1 overlaps the copy of j.  Same IDs as the GPU path (sampled on the GPU beforehand)."""
+    R = cfg.row_bytes
+    threads = max(1, (os.cpu_count() or 1) // d.world)
+    torch.set_num_threads(threads)
+    nb = min(K, 8)
+    ids = []
+    for i in range(nb):
+        mb = fetcher.fetch(seeds_dev[i], rng[i])
+        n = mb.sizes()[-1]
+        ids.append(torch.from_numpy(mb.bufs.ids[:n].cpu().numpy()))
+    host = torch.from_numpy(buf.numpy(0, cfg.table_bytes)).view(cfg.n_nodes, R)
+    cap = max(x.numel() for x in ids)
+    stage = [torch.empty((cap, R), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    dst = torch.empty((cap, R), dtype=torch.uint8, device="cuda")
+    cs = torch.cuda.Stream()
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    torch.index_select(host, 0, ids[0], out=stage[0][:ids[0].numel()])  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    total = 0
+    for i in range(nb):
+        p = i % 2
+        done[p].synchronize()
+        n = ids[i].numel()
+        torch.index_select(host, 0, ids[i], out=stage[p][:n])
+        with torch.cuda.stream(cs):
+            dst[:n].copy_(stage[p][:n], non_blocking=True)
+            done[p].record(cs)
+        total += n * R
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    return {"value": round(total / el / 1e9, 3), "unit": UNIT, "threads": threads, "minibatches": nb,
+            "how": "torch.index_select into pinned staging (T threads) + cudaMemcpyAsync, double-buffered, wall clock"}
+
+
+# ----------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands
+# ----------------------------------------------------------------------------------------------
+def run_reference(args, d: Dist):
+    import oracle
+    if d.rank != 0:
+        return None
+    cfg = gen.CONFIGS[args.config]
+    R = cfg.row_bytes
+    nbytes = cfg.table_bytes
+    raw = np.empty(nbytes + 64, dtype=np.uint8)
+    gen.fill_table(raw, nbytes, cfg.seed)
+    off, col = gen.gen_csr(cfg.n_nodes, cfg.avg_degree, cfg.seed)
+    out = np.empty(sum(gen.sample_bound(cfg.n_nodes, cfg.batch, cfg.fanouts)[-1:]) * R, dtype=np.uint8)
+    K, W = args.steps, args.warmup
+
+    def one(j):
+        seeds = gen.batch_seeds(cfg.n_nodes, cfg.batch, cfg.seed, j)
+        s, _ = oracle.sample_and_gather(off, col, seeds, cfg.fanouts, gen.batch_rng_seed(cfg.seed, j), raw.ctypes.data,
+                                        cfg.n_nodes, R, out=out)
+        return s.U.shape[0]
+    for i in range(W):
+        one(i)
+    t0 = time.perf_counter()
+    tot = 0
+    for i in range(W, W + K):
+        tot += one(i)
+    el = time.perf_counter() - t0
+    value = tot * R / el / 1e9
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": d.world,
+            "steps": K, "warmup": W, "ms_per_step": round(el / K * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 (fp32 rows moved as bytes)", "data": "synthetic",
+            "config": {"workload": f"config{cfg.cid} {cfg.name}", "global_batch": cfg.batch, "parallelism": "cpu (rank 0 only)"},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{K} config{cfg.cid} minibatches, one per step (sample + gather, single-threaded C)"},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
+    ap.add_argument("--gather-sms", type=int, default=0)
+    ap.add_argument("--gather-warps", type=int, default=0)
+    ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-overlap", dest="overlap", action="store_false")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "at least 3 warm-up steps"
+    d = Dist(args.gpus)
+    try:
+        line = run_reference(args, d) if args.impl == "reference" else run_ours(args, d)
+        if d.rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

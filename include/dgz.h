@@ -56,6 +56,8 @@ DGZ_API int dgz_abi_version(void);
 DGZ_API const char* dgz_last_error(void);
 /* Number of SMs of the current device (148 on B200), or -1. */
 DGZ_API int dgz_device_sm_count(void);
+/* Number of CUDA kernels libdgz has launched in this process (all threads, all devices). */
+DGZ_API uint64_t dgz_kernel_launches(void);
 
 /* ==========================================================================================
  * Host table manager (B1).  The paper shares one host feature table between the per-GPU
@@ -232,7 +234,9 @@ DGZ_API dgz_status dgz_sample_check(const dgz_sample_out* out, dgz_stream stream
  * node i < *n_dst_dev (bounded by n_dst_max):
  *   y[i, :] = (x[i, :] + sum_{c < cnt[i]} x[nbr_local[i*fanout + c], :]) / (1 + cnt[i])
  * over fp32 rows x [*, dim].  `repeat` re-runs the aggregation to scale the consumer's work
- * (T_c ~ T_g for the overlap measurement).  Not on the parity path.
+ * (T_c ~ T_g for the overlap measurement).  Grid: 7 CTAs x 256 threads on each of `sm_count`
+ * SMs (0 = all), leaving thread slots for a co-running gather (the MPS role of P:524-537).
+ * Not on the parity path.
  * ========================================================================================== */
 DGZ_API dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int32_t* nbr_local, const int32_t* cnt,
                               int32_t fanout, const int64_t* n_dst_dev, int64_t n_dst_max, float* y,

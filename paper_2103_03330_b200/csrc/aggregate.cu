@@ -42,9 +42,11 @@ extern "C" dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int3
     if (n_dst_max == 0) return DGZ_OK;
     const int nsm = sm_count_of_current_device();
     const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
+    // 7 CTAs of 256 threads per SM (1792 of 2048 thread slots): a co-running gather (a few
+    // 64-thread CTAs) always finds room, unlike a whole-GPU kernel (P:741-745 fig:mps_eval)
     int64_t blocks = (n_dst_max * 32 + 255) / 256;
-    const int64_t cap = (int64_t)k * 8;
+    const int64_t cap = (int64_t)k * 7;
     if (blocks > cap) blocks = cap;
-    aggregate_mean_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(x, dim, nbr_local, cnt, fanout, n_dst_dev, n_dst_max, y, repeat);
+    aggregate_mean_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(x, dim, nbr_local, cnt, fanout, n_dst_dev, n_dst_max, y, repeat); dgz::count_launch();
     return launch_check("aggregate_mean_kernel");
 }

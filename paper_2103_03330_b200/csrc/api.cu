@@ -10,6 +10,7 @@
 #include <time.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "internal.h"
@@ -37,6 +38,9 @@ int sm_count_of_current_device() {
     return n;
 }
 
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 static double now_s() {
     timespec ts;
     clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -54,6 +58,7 @@ int dgz_vmm_register(const void* p, size_t bytes);
 extern "C" int dgz_abi_version(void) { return DGZ_ABI_VERSION; }
 extern "C" const char* dgz_last_error(void) { return g_err; }
 extern "C" int dgz_device_sm_count(void) { return sm_count_of_current_device(); }
+extern "C" uint64_t dgz_kernel_launches(void) { return g_launches.load(); }
 
 // ---------------------------------------------------------------------------------------------
 // Host table manager

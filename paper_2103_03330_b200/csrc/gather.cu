@@ -222,7 +222,7 @@ struct SegLaunch {
 template <int SW, typename IdxT>
 cudaError_t launch_segment(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
     gather_segment_kernel<SW, 8, IdxT><<<L.blocks, L.threads, 0, L.s>>>(t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n,
-                                                                        L.n_dev, L.out, L.err, L.blocked);
+                                                                        L.n_dev, L.out, L.err, L.blocked); dgz::count_launch();
     return cudaGetLastError();
 }
 
@@ -243,15 +243,15 @@ cudaError_t launch_elem(const dgz_table_s* t, const IdxT* idx, int64_t n, const 
     switch (t->elem_bytes) {
         case 4:
             gather_elem_kernel<uint32_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint32_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
-                                                                           (uint32_t*)out, err);
+                                                                           (uint32_t*)out, err); dgz::count_launch();
             break;
         case 2:
             gather_elem_kernel<uint16_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint16_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
-                                                                           (uint16_t*)out, err);
+                                                                           (uint16_t*)out, err); dgz::count_launch();
             break;
         default:
             gather_elem_kernel<uint8_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint8_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
-                                                                          (uint8_t*)out, err);
+                                                                          (uint8_t*)out, err); dgz::count_launch();
     }
     return cudaGetLastError();
 }

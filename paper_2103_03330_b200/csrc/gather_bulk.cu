@@ -143,7 +143,7 @@ cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, const int64_t* ds
     cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<SW, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     gather_bulk_kernel<SW, IdxT><<<blocks, threads, smem, s>>>(t->dev, t->rows, t->row_bytes, idx, dst_pos, n, n_dev, out, err, S,
-                                                               slot_bytes, blocked);
+                                                               slot_bytes, blocked); dgz::count_launch();
     return cudaGetLastError();
 }
 

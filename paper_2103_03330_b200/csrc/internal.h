@@ -30,6 +30,7 @@ inline dgz_status launch_check(const char* what) {
 }
 
 int sm_count_of_current_device();
+void count_launch();  // every kernel launch of libdgz increments dgz_kernel_launches()
 
 }  // namespace dgz
 

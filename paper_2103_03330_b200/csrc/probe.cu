@@ -57,17 +57,17 @@ extern "C" dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t chunks = bytes / 16;
     switch (unroll) {
-        case 1: stream_kernel<1><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
-        case 2: stream_kernel<2><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
-        case 4: stream_kernel<4><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
-        case 16: stream_kernel<16><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
-        default: stream_kernel<8><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        case 1: stream_kernel<1><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); dgz::count_launch(); break;
+        case 2: stream_kernel<2><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); dgz::count_launch(); break;
+        case 4: stream_kernel<4><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); dgz::count_launch(); break;
+        case 16: stream_kernel<16><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); dgz::count_launch(); break;
+        default: stream_kernel<8><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); dgz::count_launch(); break;
     }
     return launch_check("stream_kernel");
 }
 
 extern "C" dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream) {
     DGZ_REQUIRE(src_dev && cycles_dev && steps > 0, "dgz_probe_chase: bad args");
-    chase_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const int64_t*)src_dev, steps, cycles_dev);
+    chase_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const int64_t*)src_dev, steps, cycles_dev); dgz::count_launch();
     return launch_check("chase_kernel");
 }

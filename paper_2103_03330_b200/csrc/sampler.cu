@@ -387,11 +387,11 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
     if (n_seeds > 0) {
         const int gs = grid_for(n_seeds, 256);
         const int sc = (int)((n_seeds + kSeedChunk - 1) / kSeedChunk);
-        seeds_mark_kernel<<<gs, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, err);
-        seeds_min_kernel<<<gs, 256, 0, s>>>(seeds_dev, n_seeds, N, pos);
-        seeds_count_kernel<<<sc, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, ssum);
-        scan_chunks_kernel<<<1, 1024, 0, s>>>(ssum, sc, soff, nullptr, sizes);
-        seeds_emit_kernel<<<sc, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, soff, out->ids, front);
+        seeds_mark_kernel<<<gs, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, err); dgz::count_launch();
+        seeds_min_kernel<<<gs, 256, 0, s>>>(seeds_dev, n_seeds, N, pos); dgz::count_launch();
+        seeds_count_kernel<<<sc, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, ssum); dgz::count_launch();
+        scan_chunks_kernel<<<1, 1024, 0, s>>>(ssum, sc, soff, nullptr, sizes); dgz::count_launch();
+        seeds_emit_kernel<<<sc, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, soff, out->ids, front); dgz::count_launch();
     } else {
         DGZ_CUDA(cudaMemsetAsync(sizes, 0, 8, s));
     }
@@ -408,25 +408,31 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
         else
             hop_sample_kernel<int32_t><<<gh, 256, 0, s>>>(csr->offsets, (const int32_t*)csr->cols, out->ids, sizes, k, f, k0, k1, nbr_k,
                                                           cnt_k, cand);
-        bitmap_count_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, cand, csum);
-        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, sizes + k, sizes + k + 1);
-        bitmap_emit_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, cand, coff, sizes, k, out->ids);
+        dgz::count_launch();
+        bitmap_count_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, cand, csum); dgz::count_launch();
+        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, sizes + k, sizes + k + 1); dgz::count_launch();
+        bitmap_emit_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, cand, coff, sizes, k, out->ids); dgz::count_launch();
         nbr_off += bounds[k] * f;
         cnt_off += bounds[k];
     }
-    if (out->nbr_local || out->ids_sorted) posmap_kernel<<<grid_for(bounds[n_layers], 256), 256, 0, s>>>(out->ids, sizes, n_layers, pos);
+    if (out->nbr_local || out->ids_sorted) {
+        posmap_kernel<<<grid_for(bounds[n_layers], 256), 256, 0, s>>>(out->ids, sizes, n_layers, pos);
+        dgz::count_launch();
+    }
     if (out->ids_sorted) {
         // the final frontier bitmap holds exactly U: compact it in ascending ID order
-        bitmap_count_all_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, csum);
-        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, nullptr, csum + l.nchunks);
-        bitmap_emit_sorted_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, coff, pos, out->ids_sorted, out->ids_sorted_pos);
+        bitmap_count_all_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, csum); dgz::count_launch();
+        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, nullptr, csum + l.nchunks); dgz::count_launch();
+        bitmap_emit_sorted_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, coff, pos, out->ids_sorted, out->ids_sorted_pos); dgz::count_launch();
     }
     if (out->nbr_local) {
         int64_t o = 0;
         for (int k = 0; k < n_layers; ++k) {
-            if (fanouts[k] > 0)
+            if (fanouts[k] > 0) {
                 local_kernel<<<grid_for(bounds[k] * fanouts[k], 256), 256, 0, s>>>(out->nbr + o, sizes, k, fanouts[k], pos,
                                                                                  out->nbr_local + o);
+                dgz::count_launch();
+            }
             o += bounds[k] * fanouts[k];
         }
     }

@@ -83,6 +83,7 @@ _SIGS = {
     "dgz_abi_version": ([], ctypes.c_int),
     "dgz_last_error": ([], ctypes.c_char_p),
     "dgz_device_sm_count": ([], ctypes.c_int),
+    "dgz_kernel_launches": ([], ctypes.c_uint64),
     "dgz_host_alloc": ([ctypes.c_char_p, _sz, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
     "dgz_host_free": ([_vp, _sz], ctypes.c_int),
     "dgz_host_unlink": ([ctypes.c_char_p], ctypes.c_int),
@@ -123,6 +124,10 @@ def last_error() -> str:
 
 def device_sm_count() -> int:
     return _lib.dgz_device_sm_count()
+
+
+def kernel_launches() -> int:
+    return int(_lib.dgz_kernel_launches())
 
 
 def _stream(stream) -> int:

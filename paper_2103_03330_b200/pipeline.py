@@ -1,0 +1,87 @@
+"""Per-GPU minibatch fetch pipeline (steps a2-a5): sampler -> zero-copy gather into ping-pong
+HBM buffers on a side stream, consumed on another stream (section 3.3,
+fig:singlegpu; section 3.2.2).
+
+The paper runs sampler, producer (gather) and consumer (training) as three processes and
+shares the ping-pong buffers with CUDA IPC, limiting the producer to X% of the SMs with MPS.
+On B200 one process per GPU does it with two CUDA streams and events: the fetch for step j+1
+is enqueued on ``fetch_stream`` into the other slot while the consumer works on slot j, the
+gather's grid is bounded to a few SMs (``gather_cfg.sm_count``), nothing allocates or blocks
+inside the loop, and the whole fetch (sampling + gather) runs on the device with
+the data-dependent sizes kept in device memory.  Everything compute-related is a libdgz call.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import dgz
+
+
+@dataclass
+class Minibatch:
+    slot: int
+    bufs: dgz.SampleBuffers
+    rows: torch.Tensor          # [cap, row_bytes] uint8 in HBM: row r = table[ids[r]]
+    event: torch.cuda.Event     # recorded on the fetch stream after the gather
+    fanouts: tuple
+
+    @property
+    def n_dev(self) -> torch.Tensor:
+        L = len(self.fanouts)
+        return self.bufs.sizes_dev[L:L + 1]
+
+    def wait(self, stream=None) -> None:
+        (torch.cuda.current_stream() if stream is None else stream).wait_event(self.event)
+
+    def sizes(self) -> list:
+        """|F_0..F_L| (synchronises with the fetch)."""
+        self.event.synchronize()
+        return self.bufs.sizes_host.tolist()
+
+
+class MinibatchFetcher:
+    """Owns ping-pong sample buffers and row buffers for one GPU and one registered table."""
+
+    def __init__(self, table: dgz.Table, graph: dgz.Graph, fanouts, max_seeds: int, slots: int = 2,
+                 gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None):
+        self.table, self.graph = table, graph
+        self.fanouts = tuple(int(f) for f in fanouts)
+        self.max_seeds = max_seeds
+        self.cfg = gather_cfg
+        # high priority: the gather's few CTAs are scheduled ahead of the consumer's as SMs free up
+        self.stream = torch.cuda.Stream(priority=-1) if fetch_stream is None else fetch_stream
+        self.bufs = [dgz.SampleBuffers(graph.n_nodes, max_seeds, self.fanouts, blocks=blocks, local=blocks,
+                                       sorted_ids=True) for _ in range(slots)]
+        cap = self.bufs[0].bounds[-1]
+        self.rows = [torch.empty((cap, table.row_bytes), dtype=torch.uint8, device="cuda") for _ in range(slots)]
+        self.seed_stage = [torch.empty(max_seeds, dtype=torch.int64, device="cuda") for _ in range(slots)]
+        self.events = [torch.cuda.Event() for _ in range(slots)]
+        self.free = [torch.cuda.Event() for _ in range(slots)]
+        self.next_slot = 0
+
+    def release(self, mb: Minibatch, stream=None) -> None:
+        """Mark slot `mb.slot` reusable once the consumer's queued work on `stream` is done."""
+        self.free[mb.slot].record(torch.cuda.current_stream() if stream is None else stream)
+
+    def fetch(self, seeds: torch.Tensor, rng_seed: int, slot: int | None = None) -> Minibatch:
+        """Enqueue sampling + gather of one minibatch (seeds: int64, on the device or pinned host)."""
+        p = self.next_slot if slot is None else slot
+        self.next_slot = (p + 1) % len(self.bufs)
+        s = self.stream
+        s.wait_event(self.free[p])          # never overwrite rows the consumer still reads
+        n_seeds = seeds.numel()
+        assert n_seeds <= self.max_seeds
+        with torch.cuda.stream(s):
+            if not seeds.is_cuda:
+                self.seed_stage[p][:n_seeds].copy_(seeds, non_blocking=True)   # H2D of the index list
+                seeds = self.seed_stage[p][:n_seeds]
+            b = self.bufs[p]
+            dgz.sample_uniform(self.graph, seeds, self.fanouts, rng_seed, b, stream=s)
+            cap = b.bounds[-1]
+            L = len(self.fanouts)
+            dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=cap,
+                            n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=s)
+            self.events[p].record(s)
+        return Minibatch(p, b, self.rows[p], self.events[p], self.fanouts)
