@@ -32,31 +32,43 @@ __device__ __forceinline__ uint4 ld_zc_v4(uint64_t p) {
     return r;
 }
 
+__device__ __forceinline__ void st_g(uint64_t d, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_g(uint64_t d, uint2 v) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(d), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_g32(uint64_t d, uint32_t v) { asm volatile("st.global.u32 [%0], %1;" ::"l"(d), "r"(v) : "memory"); }
+__device__ __forceinline__ void st_g16(uint64_t d, uint32_t v) {
+    asm volatile("st.global.u16 [%0], %1;" ::"l"(d), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void st_g8(uint64_t d, uint32_t v) {
+    asm volatile("st.global.u8 [%0], %1;" ::"l"(d), "h"((unsigned short)(v & 0xff)) : "memory");
+}
+
 template <int SW>
 __device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo, int hi) {
-    // store bytes [lo, hi) of the 16-byte chunk v (lo, hi multiples of SW) at d + byte
+    // store bytes [lo, hi) of the 16-byte chunk v (lo, hi multiples of SW) at global address d + byte
     if constexpr (SW == 16) {
-        *reinterpret_cast<uint4*>(d) = v;
+        st_g(d, v);
     } else if constexpr (SW == 8) {
-        const uint2 p0 = make_uint2(v.x, v.y), p1 = make_uint2(v.z, v.w);
-        if (lo <= 0 && hi >= 8) *reinterpret_cast<uint2*>(d) = p0;
-        if (lo <= 8 && hi >= 16) *reinterpret_cast<uint2*>(d + 8) = p1;
+        if (lo <= 0 && hi >= 8) st_g(d, make_uint2(v.x, v.y));
+        if (lo <= 8 && hi >= 16) st_g(d + 8, make_uint2(v.z, v.w));
     } else if constexpr (SW == 4) {
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int p = 0; p < 4; ++p)
-            if (p * 4 >= lo && p * 4 < hi) *reinterpret_cast<uint32_t*>(d + 4 * p) = w[p];
+            if (p * 4 >= lo && p * 4 < hi) st_g32(d + 4 * p, w[p]);
     } else if constexpr (SW == 2) {
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int p = 0; p < 8; ++p)
-            if (p * 2 >= lo && p * 2 < hi)
-                *reinterpret_cast<uint16_t*>(d + 2 * p) = (uint16_t)(w[p >> 1] >> (16 * (p & 1)));
+            if (p * 2 >= lo && p * 2 < hi) st_g16(d + 2 * p, w[p >> 1] >> (16 * (p & 1)));
     } else {
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int p = 0; p < 16; ++p)
-            if (p >= lo && p < hi) *reinterpret_cast<uint8_t*>(d + p) = (uint8_t)(w[p >> 2] >> (8 * (p & 3)));
+            if (p >= lo && p < hi) st_g8(d + p, w[p >> 2] >> (8 * (p & 3)));
     }
 }
 
