@@ -45,9 +45,13 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.same_device = os.environ.get("DGZ_BENCH_SAME_DEVICE") == "1"  # N ranks on one GPU (test only)
+        if self.same_device:
+            self.local = 0
         if self.world > 1:
             import torch.distributed as dist
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = "nccl" if (torch.cuda.is_available() and not self.same_device) else "gloo"
+            self.backend = backend
             if torch.cuda.is_available():
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend=backend)
@@ -59,7 +63,7 @@ class Dist:
 
     def barrier(self):
         if self.pg:
-            if torch.cuda.is_available():
+            if self.backend == "nccl":
                 self.pg.barrier(device_ids=[self.local])
             else:
                 self.pg.barrier()
@@ -67,7 +71,7 @@ class Dist:
     def allreduce(self, vals, op="sum"):
         if not self.pg:
             return list(vals)
-        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        dev = "cuda" if self.backend == "nccl" else "cpu"
         t = torch.tensor(vals, dtype=torch.float64, device=dev)
         self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM if op == "sum" else self.pg.ReduceOp.MAX)
         return t.cpu().tolist()
@@ -204,15 +208,16 @@ def measure_ceilings(dgz, table_info, R):
 
 
 def load_profile_traffic(cid):
-    """dram bytes per gather launch from the committed ncu --set full summary, if present."""
+    """(dram bytes per gather launch, summary) from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_gather_summary.json")
     try:
         with open(p) as f:
-            j = json.load(f)
-        c = j.get(f"config{cid}")
-        return c if c else None
+            c = json.load(f).get(f"config{cid}")
+        if not c:
+            return None, None
+        return int(c["dram_bytes_per_launch"]), {k: v for k, v in c.items() if k != "launches"}
     except Exception:
-        return None
+        return None, None
 
 
 # ----------------------------------------------------------------------------------------------
@@ -243,7 +248,8 @@ def run_ours(args, d: Dist):
     seeds_dev = [x.cuda() for x in seeds_host]
     rng = [gen.batch_rng_seed(cfg.seed, j) for j in batches]
 
-    gcfg = dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps)
+    gcfg = dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps) if (args.gather_sms or args.gather_warps) else None
+    sm_count_all = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True)
     cap = fetcher.bufs[0].bounds[-1]
     n_steps = torch.zeros(W + K, dtype=torch.int64, device="cuda")
@@ -317,7 +323,7 @@ def run_ours(args, d: Dist):
 
     clocks = clk.summary()
     sm_count = torch.cuda.get_device_properties(0).multi_processor_count
-    traffic = load_profile_traffic(cfg.cid)
+    traffic, traffic_detail = load_profile_traffic(cfg.cid)
     peak = ceilings["h2d_dma_gbs"]
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": G, "steps": K, "warmup": W,
@@ -329,11 +335,12 @@ def run_ours(args, d: Dist):
                                f"{cfg.batch} seeds per GPU per step",
                    "global_batch": cfg.batch * G, "parallelism": f"dp{G} (seed partition j mod G)",
                    "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
-                   "gather": {"variant": "segment", "sm_count": args.gather_sms or 96,
-                              "warps_per_cta": args.gather_warps or 2, "order": "address-sorted + inverse permutation"}},
+                   "gather": {"variant": "segment", "sm_count": args.gather_sms or sm_count_all,
+                              "warps_per_cta": args.gather_warps or 2, "lines_in_flight_per_warp": 64,
+                              "order": "address-sorted + inverse permutation"}},
         "per_gpu_gbs": round(per_gpu, 3),
         "roofline": {"bound": "pcie", "achieved": round(gather_gbs, 3), "peak": peak, "unit": "GB/s",
-                     "frac": round(gather_gbs / peak, 4), "traffic": traffic,
+                     "frac": round(gather_gbs / peak, 4), "traffic": traffic, "traffic_detail": traffic_detail,
                      "kernel": "gather_segment_kernel (dgz_gather_perm)",
                      "peak_source": "measured in this run: cudaMemcpyAsync H2D from pinned memory (PCIe Gen5 x16); "
                                     "MEASURED_PEAKS.json has no PCIe figure",
@@ -391,84 +398,93 @@ def run_e2e(fetcher, cfg, seeds_host, rng, W, K, d: Dist):
 
 
 def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
-    """Exposed fetch time with a stand-in GraphSAGE mean-aggregation consumer (a5-a7), and the
-    gather-SM sweep (a6: the B200 analogue of the paper's MPS ratio sweep, fig:mps_bandwidth)."""
+    """Exposed fetch time with a stand-in GraphSAGE mean-aggregation consumer (a5-a7) and the
+    SM-partition sweep (a6; the B200 analogue of the paper's MPS ratio sweep, fig:mps_bandwidth):
+    the fetch runs on a green-context partition of k SMs (dgz_partition, spread over the GPCs),
+    the consumer on the other 148 - k, and step j+1 is fetched while step j is consumed."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
     dim = cfg.dim
     L = len(cfg.fanouts)
-    comp = torch.cuda.Stream()
-    y = torch.empty((fetcher.bufs[0].bounds[L - 1], dim), dtype=torch.float32, device="cuda")
-    nstep = min(K, 10)
-    nb = sum(fetcher.bufs[0].bounds[k] * cfg.fanouts[k] for k in range(L - 1))
-    cb = sum(fetcher.bufs[0].bounds[k] for k in range(L - 1))
-    a, b = ev(), ev()
-    saved = fetcher.cfg
+    nstep = min(K, 8)
+    ev2 = (ev(), ev())
 
-    def consume(mb, repeat):
+    def consume(comp, mb, repeat, y, nb, cb):
         dgz.aggregate_mean(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:], cfg.fanouts[L - 1],
-                           mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], y, repeat=repeat, sm_count=0, stream=comp)
+                           mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], y, repeat=repeat, stream=comp)
 
-    def fetch_alone():
+    def measure(f, comp, repeat=None, t_target=None):
+        y = torch.empty((f.bufs[0].bounds[L - 1], dim), dtype=torch.float32, device="cuda")
+        nb = sum(f.bufs[0].bounds[k] * cfg.fanouts[k] for k in range(L - 1))
+        cb = sum(f.bufs[0].bounds[k] for k in range(L - 1))
+        a, b = ev2
         for i in range(2):
-            fetcher.fetch(seeds_dev[i], rng[i])
+            f.fetch(seeds_dev[i], rng[i])
         torch.cuda.synchronize()
-        a.record(fetcher.stream)
+        a.record(f.stream)
         for i in range(nstep):
-            fetcher.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)])
-        b.record(fetcher.stream)
+            f.fetch(seeds_dev[i], rng[i])
+        b.record(f.stream)
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / nstep
+        t_g = a.elapsed_time(b) / nstep
+        mb = f.fetch(seeds_dev[0], rng[0])
+        mb.event.synchronize()
 
-    def consumer_alone(mb, repeat):
-        with torch.cuda.stream(comp):
+        def cons_alone(rep):
+            torch.cuda.synchronize()
             a.record(comp)
             for _ in range(nstep):
-                consume(mb, repeat)
+                consume(comp, mb, rep, y, nb, cb)
             b.record(comp)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / nstep
+        if repeat is None:
+            repeat = 8
+            for _ in range(3):
+                repeat = max(1, int(round(repeat * (t_target or t_g) / cons_alone(repeat))))
+        t_c = cons_alone(repeat)
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / nstep
-
-    def pipelined(repeat):
-        torch.cuda.synchronize()
-        mbs = [fetcher.fetch(seeds_dev[0], rng[0])]
-        start, end = ev(), ev()
-        start.record(comp)
+        mbs = [f.fetch(seeds_dev[0], rng[0])]
+        a.record(comp)
         for i in range(1, nstep + 1):
-            nxt = fetcher.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)])
+            nxt = f.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)])
             cur = mbs[-1]
             comp.wait_event(cur.event)
-            with torch.cuda.stream(comp):
-                consume(cur, repeat)
-            fetcher.release(cur, comp)
+            consume(comp, cur, repeat, y, nb, cb)
+            f.release(cur, comp)
             mbs.append(nxt)
         comp.wait_event(mbs[-1].event)
-        end.record(comp)
+        b.record(comp)
         torch.cuda.synchronize()
-        return start.elapsed_time(end) / nstep
+        t_o = a.elapsed_time(b) / nstep
+        return t_g, t_c, t_o, repeat
 
-    # calibrate the consumer to T_c ~ T_g of the default gather
-    fetcher.cfg = dgz.gather_cfg()
-    t_g0 = fetch_alone()
-    mb = fetcher.fetch(seeds_dev[0], rng[0])
-    mb.event.synchronize()
-    repeat = 8
-    for _ in range(3):
-        t_c = consumer_alone(mb, repeat)
-        repeat = max(1, int(round(repeat * t_g0 / t_c)))
-    t_c = consumer_alone(mb, repeat)
-    sweep = []
-    for sms, warps in ((8, 4), (16, 4), (24, 2), (48, 2), (96, 2), (148, 2)):
-        fetcher.cfg = dgz.gather_cfg(sm_count=sms, warps_per_cta=warps)
-        t_g = fetch_alone()
-        t_o = pipelined(repeat)
-        sweep.append({"gather_sms": sms, "warps": warps, "t_fetch_ms": round(t_g, 3), "t_step_overlapped_ms": round(t_o, 3),
-                      "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
-                      "fetch_gbs_alone": round(float(fetcher.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2)})
+    saved = fetcher.cfg
+    fetcher.cfg = None
+    comp0 = torch.cuda.Stream()
+    t_g0, t_c0, t_o0, repeat = measure(fetcher, comp0)
     fetcher.cfg = saved
-    best = min(sweep, key=lambda r: r["t_step_overlapped_ms"])
-    return {"t_fetch_ms": round(t_g0, 3), "t_consumer_ms": round(t_c, 3), "consumer_repeat": repeat,
-            "serial_ms": round(t_g0 + t_c, 3), "best": best,
-            "hidden_frac": round(1 - best["exposed_fetch_ms"] / best["t_fetch_ms"], 3), "sm_sweep": sweep,
-            "consumer": "dgz_aggregate_mean over the last hop's block (7 CTAs x 256 thr per SM), repeated to T_c ~ T_g"}
+    rows = [{"partition": "none (whole GPU, high-priority fetch stream)", "fetch_sms": 148, "t_fetch_ms": round(t_g0, 3),
+             "t_consumer_ms": round(t_c0, 3), "t_step_overlapped_ms": round(t_o0, 3),
+             "exposed_fetch_ms": round(max(0.0, t_o0 - t_c0), 3)}]
+    for k in (4, 8, 16, 32):
+        try:
+            part = dgz.Partition(k, -1, dgz.PARTITION_SPREAD)
+        except Exception as e:  # green contexts unavailable: report and skip
+            rows.append({"fetch_sms": k, "error": str(e)[:200]})
+            continue
+        f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream)
+        t_g, t_c, t_o, _ = measure(f, part.compute_stream, repeat=repeat)
+        rows.append({"partition": "green context", "fetch_sms": part.fetch_sms, "compute_sms": part.compute_sms,
+                     "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
+                     "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
+                     "fetch_gbs_alone": round(float(f.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2)})
+        del f
+        torch.cuda.synchronize()
+        part.destroy()
+    best = min((r for r in rows if "t_step_overlapped_ms" in r), key=lambda r: r["t_step_overlapped_ms"])
+    return {"t_fetch_ms": round(t_g0, 3), "consumer_repeat": repeat, "serial_ms": round(t_g0 + t_c0, 3), "best": best,
+            "hidden_frac_best": round(1 - best["exposed_fetch_ms"] / t_g0, 3), "sweep": rows,
+            "consumer": "dgz_aggregate_mean over the last hop's block, non-persistent launches, repeated to T_c ~ T_fetch"}
 
 
 def run_oracle_leg(cfg, table_addr, graph, last, d: Dist):

@@ -66,6 +66,10 @@ DGZ_API uint64_t dgz_kernel_launches(void);
  * ========================================================================================== */
 #define DGZ_HOST_HUGEPAGE 1u /* madvise(MADV_HUGEPAGE) on the mapping */
 #define DGZ_HOST_POPULATE 2u /* pre-fault every page at creation */
+#define DGZ_HOST_CUDA_PINNED 8u /* cudaHostAlloc(Mapped | Portable): driver-allocated pinned memory
+                                   (single process; not shareable by name) */
+#define DGZ_HOST_HUGETLB_2M 16u /* anonymous MAP_HUGETLB 2 MiB pages (needs vm.nr_hugepages) */
+#define DGZ_HOST_HUGETLB_1G 32u /* anonymous MAP_HUGETLB 1 GiB pages */
 #define DGZ_HOST_VMM 4u      /* CUDA VMM host allocation (cuMemCreate on host NUMA node 0): pinned,
                                 CPU-accessible, mapped into the current GPU with large pages at the
                                 same address.  Needs a CUDA device; shm_name must be NULL (share it
@@ -155,8 +159,10 @@ typedef struct {
     int32_t warps_per_cta; /* 0 = default */
     int32_t ctas_per_sm;   /* 0 = default (1) */
     int32_t schedule;      /* dgz_gather_schedule */
-    int32_t reserved;
+    int32_t flags;         /* DGZ_GATHER_FLAG_* (SEGMENT variant) */
 } dgz_gather_cfg;
+#define DGZ_GATHER_FLAG_L2_EVICT_FIRST 1 /* zero-copy loads with an L2 evict-first cache policy */
+#define DGZ_GATHER_FLAG_DEEP 2           /* 16 instead of 8 line loads in flight per lane */
 
 /* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
  * gathers min(*n_dev, n) rows (n is the capacity), so a gather can follow the sampler on the
@@ -234,13 +240,32 @@ DGZ_API dgz_status dgz_sample_check(const dgz_sample_out* out, dgz_stream stream
  * node i < *n_dst_dev (bounded by n_dst_max):
  *   y[i, :] = (x[i, :] + sum_{c < cnt[i]} x[nbr_local[i*fanout + c], :]) / (1 + cnt[i])
  * over fp32 rows x [*, dim].  `repeat` re-runs the aggregation to scale the consumer's work
- * (T_c ~ T_g for the overlap measurement).  Grid: 7 CTAs x 256 threads on each of `sm_count`
- * SMs (0 = all), leaving thread slots for a co-running gather (the MPS role of P:524-537).
+ * (T_c ~ T_g for the overlap measurement).  ctas_per_sm == 0: `repeat` launches of a
+ * non-persistent grid (one 256-thread CTA per 8 destination nodes; short-lived CTAs, like training
+ * kernels, so a co-running fetch gets SM slots quickly).  ctas_per_sm > 0: one persistent launch of
+ * ctas_per_sm x sm_count CTAs (sm_count 0 = all) that holds its slots for the whole call.
  * Not on the parity path.
  * ========================================================================================== */
 DGZ_API dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int32_t* nbr_local, const int32_t* cnt,
                               int32_t fanout, const int64_t* n_dst_dev, int64_t n_dst_max, float* y,
-                              int32_t repeat, int32_t sm_count, dgz_stream stream);
+                              int32_t repeat, int32_t sm_count, int32_t ctas_per_sm, dgz_stream stream);
+
+/* ==========================================================================================
+ * In-process SM partition (step a6): the paper's MPS X% / (100-X)% split done with
+ * CUDA green contexts.  The current device's SMs are split into a fetch group of at least
+ * `fetch_sms` SMs (rounded up to the hardware granularity: multiples of 8 on sm_90+, finer with
+ * DGZ_PARTITION_FINE) and a compute group with the rest; each group gets one non-blocking stream.
+ * Kernels launched on a group's stream run only on that group's SMs.  Device memory of the
+ * primary context is usable from both.  Destroy after all work on the streams has finished.
+ * ========================================================================================== */
+typedef struct dgz_partition_s* dgz_partition;
+#define DGZ_PARTITION_FINE 1u   /* CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING: finer SM counts */
+#define DGZ_PARTITION_SPREAD 2u /* fetch SMs taken evenly across the device (all GPCs) from the
+                                   finest split; the compute group gets every other SM */
+DGZ_API dgz_status dgz_partition_create(int32_t fetch_sms, int32_t fetch_priority, uint32_t flags, dgz_partition* out);
+DGZ_API dgz_status dgz_partition_get(dgz_partition p, dgz_stream* fetch_stream, dgz_stream* compute_stream,
+                                     int32_t* fetch_sms, int32_t* compute_sms);
+DGZ_API dgz_status dgz_partition_destroy(dgz_partition p);
 
 /* ==========================================================================================
  * PCIe probes (the zero-copy ceiling and the round-trip time).

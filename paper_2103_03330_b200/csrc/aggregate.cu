@@ -36,17 +36,29 @@ using namespace dgz;
 
 extern "C" dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int32_t* nbr_local, const int32_t* cnt, int32_t fanout,
                                          const int64_t* n_dst_dev, int64_t n_dst_max, float* y, int32_t repeat, int32_t sm_count,
-                                         dgz_stream stream) {
+                                         int32_t ctas_per_sm, dgz_stream stream) {
     DGZ_REQUIRE(x && nbr_local && cnt && y && dim >= 1 && fanout >= 0 && n_dst_max >= 0 && repeat >= 1,
                 "dgz_aggregate_mean: bad arguments");
     if (n_dst_max == 0) return DGZ_OK;
     const int nsm = sm_count_of_current_device();
     const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
-    // 7 CTAs of 256 threads per SM (1792 of 2048 thread slots): a co-running gather (a few
-    // 64-thread CTAs) always finds room, unlike a whole-GPU kernel (P:741-745 fig:mps_eval)
+    // ctas_per_sm == 0: non-persistent grid (one CTA per 8 destination nodes, each CTA lives a few
+    // microseconds, like training kernels), launched `repeat` times: a high-priority fetch stream
+    // gets SM slots within microseconds.  ctas_per_sm > 0: a persistent grid of k * ctas_per_sm
+    // CTAs doing all repeats in one launch (occupies its slots for the whole call).
     int64_t blocks = (n_dst_max * 32 + 255) / 256;
-    const int64_t cap = (int64_t)k * 7;
-    if (blocks > cap) blocks = cap;
-    aggregate_mean_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(x, dim, nbr_local, cnt, fanout, n_dst_dev, n_dst_max, y, repeat); dgz::count_launch();
+    if (ctas_per_sm > 0) {
+        const int64_t cap = (int64_t)k * ctas_per_sm;
+        if (blocks > cap) blocks = cap;
+        aggregate_mean_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(x, dim, nbr_local, cnt, fanout, n_dst_dev, n_dst_max, y,
+                                                                            repeat);
+        dgz::count_launch();
+    } else {
+        for (int r = 0; r < repeat; ++r) {
+            aggregate_mean_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(x, dim, nbr_local, cnt, fanout, n_dst_dev, n_dst_max,
+                                                                                y, 1);
+            dgz::count_launch();
+        }
+    }
     return launch_check("aggregate_mean_kernel");
 }

@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <map>
 
 #include "internal.h"
 
@@ -51,6 +52,9 @@ static double now_s() {
 
 using namespace dgz;
 
+static std::mutex g_pinned_mu;
+static std::map<uintptr_t, size_t> g_pinned;  // cudaHostAlloc'ed host tables -> bytes
+
 dgz_status dgz_vmm_alloc(size_t bytes, void** ptr);
 int dgz_vmm_free(void* ptr);
 int dgz_vmm_register(const void* p, size_t bytes);
@@ -70,9 +74,22 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
         DGZ_REQUIRE(!shm_name, "dgz_host_alloc: DGZ_HOST_VMM allocations are shared with dgz_host_export, not by name");
         return dgz_vmm_alloc(bytes, ptr);
     }
+    if (flags & DGZ_HOST_CUDA_PINNED) {
+        DGZ_REQUIRE(!shm_name, "dgz_host_alloc: DGZ_HOST_CUDA_PINNED memory cannot be named");
+        void* p = nullptr;
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+        std::lock_guard<std::mutex> g(g_pinned_mu);
+        g_pinned[(uintptr_t)p] = bytes;
+        *ptr = p;
+        return DGZ_OK;
+    }
     void* p = MAP_FAILED;
     if (!shm_name) {
-        p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        int extra = 0;
+        if (flags & DGZ_HOST_HUGETLB_2M) extra = MAP_HUGETLB | (21 << MAP_HUGE_SHIFT);
+        if (flags & DGZ_HOST_HUGETLB_1G) extra = MAP_HUGETLB | (30 << MAP_HUGE_SHIFT);
+        p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | extra, -1, 0);
     } else {
         DGZ_REQUIRE(shm_name[0] == '/', "dgz_host_alloc: shm name must start with '/'");
         int fd = shm_open(shm_name, O_RDWR | (create ? O_CREAT : 0), 0600);
@@ -108,6 +125,14 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
 extern "C" dgz_status dgz_host_free(void* ptr, size_t bytes) {
     DGZ_REQUIRE(ptr && bytes > 0, "dgz_host_free: null ptr or zero size");
     if (dgz_vmm_free(ptr) == 1) return DGZ_OK;
+    {
+        std::lock_guard<std::mutex> g(g_pinned_mu);
+        if (g_pinned.erase((uintptr_t)ptr)) {
+            cudaError_t e = cudaFreeHost(ptr);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFreeHost");
+            return DGZ_OK;
+        }
+    }
     if (munmap(ptr, bytes) != 0) { set_error("munmap: %s", strerror(errno)); return DGZ_ERR_INVALID; }
     return DGZ_OK;
 }
@@ -132,6 +157,14 @@ static int elem_bytes_of(dgz_dtype d) {
         case DGZ_U8: return 1;
     }
     return 0;
+}
+
+static bool is_cuda_pinned(const void* p) {
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    auto it = g_pinned.upper_bound((uintptr_t)p);
+    if (it == g_pinned.begin()) return false;
+    --it;
+    return (uintptr_t)p >= it->first && (uintptr_t)p < it->first + it->second;
 }
 
 extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int64_t dim, dgz_dtype dtype,
@@ -172,7 +205,7 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
     }
     if (vmm == 1) {
         t->flags |= DGZ_REG_NO_PIN | DGZ_REG_VMM_BACKED;  // CUDA VMM host memory: already mapped
-    } else if (!(flags & DGZ_REG_NO_PIN)) {
+    } else if (!(flags & DGZ_REG_NO_PIN) && !is_cuda_pinned(host_ptr)) {
         unsigned int rf = cudaHostRegisterMapped;
         if (flags & DGZ_REG_PORTABLE) rf |= cudaHostRegisterPortable;
         if (flags & DGZ_REG_READONLY) {

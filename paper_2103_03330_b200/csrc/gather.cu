@@ -31,6 +31,19 @@ __device__ __forceinline__ uint4 ld_zc_v4(uint64_t p) {
                  : "l"(p));
     return r;
 }
+// same with an L2 evict-first cache policy (keeps the GPU page-table lines resident in L2)
+__device__ __forceinline__ uint4 ld_zc_v4_ef(uint64_t p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 
 __device__ __forceinline__ void st_g(uint64_t d, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
@@ -72,8 +85,8 @@ __device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo,
     }
 }
 
-template <int SW, int U, typename IdxT>
-__global__ void __launch_bounds__(1024, 1)
+template <int SW, int U, bool HINT, typename IdxT>
+__global__ void __launch_bounds__(512, 1)
 gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
                       const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
                       uint8_t* __restrict__ dst, int* __restrict__ err, int blocked) {
@@ -87,6 +100,7 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
     const int sub = lane & 7;
     const uint64_t base = reinterpret_cast<uint64_t>(src);
     const uint64_t dbase = reinterpret_cast<uint64_t>(dst);
+    const uint64_t pol = HINT ? policy_evict_first() : 0;
 
     // Schedule of 32-row batches.  Interleaved: warp w of the grid takes batches w, w + W, ...
     // Blocked (translation-aware): CTA c owns a contiguous range of batches and its warps
@@ -164,7 +178,7 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                 const int cq = (t - er) * 128 + sub * 16 - q;  // chunk start relative to the row start
                 const bool act = (t < T) && (cq + 16 > 0) && (cq < (int)R);
                 pk[u] = act ? (((cq + 128) << 5) | sl) : -1;
-                if (act) v[u] = ld_zc_v4(ar + (uint64_t)(int64_t)cq);
+                if (act) v[u] = HINT ? ld_zc_v4_ef(ar + (uint64_t)(int64_t)cq, pol) : ld_zc_v4(ar + (uint64_t)(int64_t)cq);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -222,6 +236,7 @@ gather_elem_kernel(const T* __restrict__ src, int64_t rows, int64_t F, const Idx
 }
 
 struct SegLaunch {
+    int flags;
     const int64_t* dst_pos;
     int64_t n;
     const int64_t* n_dev;
@@ -231,10 +246,24 @@ struct SegLaunch {
     cudaStream_t s;
 };
 
+template <int SW, int U, bool HINT, typename IdxT>
+void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
+    gather_segment_kernel<SW, U, HINT, IdxT><<<L.blocks, L.threads, 0, L.s>>>(t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n,
+                                                                              L.n_dev, L.out, L.err, L.blocked);
+    dgz::count_launch();
+}
+
 template <int SW, typename IdxT>
 cudaError_t launch_segment(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
-    gather_segment_kernel<SW, 8, IdxT><<<L.blocks, L.threads, 0, L.s>>>(t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n,
-                                                                        L.n_dev, L.out, L.err, L.blocked); dgz::count_launch();
+    const bool hint = L.flags & DGZ_GATHER_FLAG_L2_EVICT_FIRST;
+    const bool deep = L.flags & DGZ_GATHER_FLAG_DEEP;
+    if (deep) {
+        if (hint) launch_segment_k<SW, 16, true>(t, idx, L);
+        else launch_segment_k<SW, 16, false>(t, idx, L);
+    } else {
+        if (hint) launch_segment_k<SW, 8, true>(t, idx, L);
+        else launch_segment_k<SW, 8, false>(t, idx, L);
+    }
     return cudaGetLastError();
 }
 
@@ -305,10 +334,13 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     // (dgz_gather_perm): a narrow in-flight window (~200 warps x 8 rows) keeps translations
     // local and still covers the PCIe bandwidth-delay product; it also leaves SMs free.
     const bool sorted_path = dst_pos != nullptr;
-    int k = bounded ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : (sorted_path && nsm > 96 ? 96 : nsm);
+    int k = bounded ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : nsm;
     int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta
                                                 : (variant == DGZ_GATHER_BULK ? 8 : (sorted_path ? 2 : 16));
-    if (warps > 32) warps = 32;
+    int flags = cfg ? cfg->flags : 0;
+    if (sorted_path && !bounded && !(cfg && cfg->warps_per_cta > 0) && flags == 0) flags = DGZ_GATHER_FLAG_DEEP;
+    const int max_warps = variant == DGZ_GATHER_SEGMENT ? 16 : 32;  // SEGMENT: <= 512 threads (128 regs)
+    if (warps > max_warps) warps = max_warps;
     int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : 1;
     if (warps * cps > 64) cps = 64 / warps > 0 ? 64 / warps : 1;
     const int sched = cfg ? cfg->schedule : DGZ_SCHED_AUTO;
@@ -325,7 +357,7 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
         if (blocks > need) blocks = need;
         const uint64_t x = (uint64_t)t->row_bytes | ((uint64_t)(uintptr_t)t->dev & 15u) | ((uint64_t)(uintptr_t)out & 15u) | 16u;
         const int sw = (int)(x & (~x + 1));
-        SegLaunch L{dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s};
+        SegLaunch L{flags, dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s};
         if (idx_is64)
             e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, L);
         else

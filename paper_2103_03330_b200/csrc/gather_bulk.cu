@@ -89,10 +89,13 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
     const uint64_t base = reinterpret_cast<uint64_t>(src);
 
     if (warp == 0) {
-        // producer warp: lane l issues jobs j = l, l + 32, ...  (each job's slot is private)
-        for (int64_t j0 = 0; j0 < njobs; j0 += 32) {
+        // producer warp: per round, lanes l < step issue jobs j0 + l (step <= S, so a slot is used
+        // at most once per round); __syncwarp keeps every lane in the same round, so an
+        // empty-barrier wait is never more than one phase ahead (parity waits are ABA-safe)
+        const int step = S < 32 ? S : 32;
+        for (int64_t j0 = 0; j0 < njobs; j0 += step) {
             const int64_t j = j0 + lane;
-            if (j < njobs) {
+            if (lane < step && j < njobs) {
                 const int s = (int)(j % S);
                 const int64_t use = j / S;
                 if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
@@ -111,6 +114,7 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
                     bulk_g2s(slots + (size_t)s * slot_bytes, a16, span, &full[s]);
                 }
             }
+            __syncwarp();
         }
     } else {
         using P = typename piece_t<SW>::T;

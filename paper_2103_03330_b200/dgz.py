@@ -24,9 +24,10 @@ _lib = ctypes.CDLL(_SO)
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_RANGE, ERR_STATE = range(6)
 F32, F16, BF16, U8 = range(4)
 REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED = 1, 2, 4, 8
-HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM = 1, 2, 4
+HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM, HOST_CUDA_PINNED, HOST_HUGETLB_2M, HOST_HUGETLB_1G = 1, 2, 4, 8, 16, 32
 GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
 SCHED_AUTO, SCHED_INTERLEAVED, SCHED_BLOCKED = range(3)
+FLAG_L2_EVICT_FIRST, FLAG_DEEP = 1, 2
 MAX_FANOUT, MAX_LAYERS = 64, 8
 ELEM_BYTES = {F32: 4, F16: 2, BF16: 2, U8: 1}
 TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16, U8: torch.uint8}
@@ -59,7 +60,7 @@ class TableInfo(ctypes.Structure):
 
 class GatherCfg(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("sm_count", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
-                ("ctas_per_sm", ctypes.c_int32), ("schedule", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("ctas_per_sm", ctypes.c_int32), ("schedule", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
 class Csr(ctypes.Structure):
@@ -101,7 +102,10 @@ _SIGS = {
     "dgz_sample_workspace_bytes": ([_i64, _i64, _P(_sz)], ctypes.c_int),
     "dgz_sample_uniform": ([_P(Csr), _vp, _i64, _P(_i32), ctypes.c_int, _u64, _P(SampleOut), _vp], ctypes.c_int),
     "dgz_sample_check": ([_P(SampleOut), _vp], ctypes.c_int),
-    "dgz_aggregate_mean": ([_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _i32, _vp], ctypes.c_int),
+    "dgz_aggregate_mean": ([_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp], ctypes.c_int),
+    "dgz_partition_create": ([_i32, _i32, _u32, _P(_vp)], ctypes.c_int),
+    "dgz_partition_get": ([_vp, _P(_vp), _P(_vp), _P(_i32), _P(_i32)], ctypes.c_int),
+    "dgz_partition_destroy": ([_vp], ctypes.c_int),
     "dgz_probe_stream": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
 }
@@ -232,8 +236,8 @@ def unregister_table(t: Table) -> None:
 
 # --- gather ------------------------------------------------------------------------------------
 def gather_cfg(variant: int = GATHER_AUTO, sm_count: int = 0, warps_per_cta: int = 0, ctas_per_sm: int = 0,
-               schedule: int = SCHED_AUTO) -> GatherCfg:
-    return GatherCfg(variant, sm_count, warps_per_cta, ctas_per_sm, schedule, 0)
+               schedule: int = SCHED_AUTO, flags: int = 0) -> GatherCfg:
+    return GatherCfg(variant, sm_count, warps_per_cta, ctas_per_sm, schedule, flags)
 
 
 def gather(table: Table, idx: torch.Tensor, out: torch.Tensor, n: int | None = None, n_dev: torch.Tensor | None = None,
@@ -348,12 +352,38 @@ def sample_check(bufs: SampleBuffers, stream=None) -> None:
     _check(_lib.dgz_sample_check(ctypes.byref(bufs.struct), _stream(stream)), "dgz_sample_check")
 
 
+# --- SM partition (green contexts) ----------------------------------------------------------------
+PARTITION_FINE, PARTITION_SPREAD = 1, 2
+
+
+class Partition:
+    """Fetch / compute SM groups with one stream each (dgz_partition_*); streams are exposed as
+    torch.cuda.ExternalStream so PyTorch work can be queued on the compute group."""
+
+    def __init__(self, fetch_sms: int, fetch_priority: int = -1, flags: int = 0):
+        h = _vp()
+        _check(_lib.dgz_partition_create(fetch_sms, fetch_priority, flags, ctypes.byref(h)), "dgz_partition_create")
+        self.handle = h.value
+        fs, cs, fn, cn = _vp(), _vp(), _i32(), _i32()
+        _check(_lib.dgz_partition_get(self.handle, ctypes.byref(fs), ctypes.byref(cs), ctypes.byref(fn), ctypes.byref(cn)),
+               "dgz_partition_get")
+        self.fetch_sms, self.compute_sms = fn.value, cn.value
+        self.fetch_stream = torch.cuda.ExternalStream(fs.value)
+        self.compute_stream = torch.cuda.ExternalStream(cs.value)
+
+    def destroy(self) -> None:
+        if self.handle:
+            torch.cuda.synchronize()
+            _check(_lib.dgz_partition_destroy(self.handle), "dgz_partition_destroy")
+            self.handle = None
+
+
 # --- stand-in consumer, probes -------------------------------------------------------------------
 def aggregate_mean(x: torch.Tensor, dim: int, nbr_local: torch.Tensor, cnt: torch.Tensor, fanout: int,
                    n_dst_dev: torch.Tensor | None, n_dst_max: int, y: torch.Tensor, repeat: int = 1, sm_count: int = 0,
-                   stream=None) -> torch.Tensor:
+                   ctas_per_sm: int = 0, stream=None) -> torch.Tensor:
     _check(_lib.dgz_aggregate_mean(_dptr(x), dim, _dptr(nbr_local), _dptr(cnt), fanout, _dptr(n_dst_dev), n_dst_max,
-                                   _dptr(y), repeat, sm_count, _stream(stream)), "dgz_aggregate_mean")
+                                   _dptr(y), repeat, sm_count, ctas_per_sm, _stream(stream)), "dgz_aggregate_mean")
     return y
 
 

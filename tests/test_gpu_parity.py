@@ -309,3 +309,60 @@ def test_step_sorted_gather_matches_oracle(dev, cid):
             assert np.array_equal(out[:n * c.row_bytes].cpu().numpy().reshape(n, -1), exp)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("R,sms,warps,n", [(4096, 4, 8, 6000), (16384, 2, 4, 1500), (65536, 1, 4, 300), (512, 1, 2, 50000)])
+def test_bulk_ring_wraparound(dev, R, sms, warps, n):
+    """BULK: many more rows per CTA than ring slots (slot reuse across many mbarrier phases),
+    rows up to 64 KiB (ring of 3 slots), rows ending exactly at the end of the registered table."""
+    rows = max(n // 2, 8)
+    t = HostTable(rows, R, seed=R + n, dtype=dgz.F32)
+    try:
+        idx = np.concatenate([np.arange(rows, dtype=np.int64), gen.random_ids(rows, n - rows, seed=R)])
+        want, _ = oracle.gather(t.np, R, idx)
+        for flags in (0,):
+            got = _gather_dev(t, idx, cfg=dgz.gather_cfg(variant=dgz.GATHER_BULK, sm_count=sms, warps_per_cta=warps))
+            assert np.array_equal(got, want)
+    finally:
+        t.close()
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+def test_segment_flags(dev, flags):
+    R, rows = 520, 5000
+    t = HostTable(rows, R, seed=flags, base=8, dtype=dgz.F32)
+    try:
+        idx = gen.random_ids(rows, 3000, seed=flags)
+        want, _ = oracle.gather(t.np, R, idx)
+        for sms, warps in ((0, 0), (3, 2), (148, 16)):
+            got = _gather_dev(t, idx, cfg=dgz.gather_cfg(sm_count=sms, warps_per_cta=warps, flags=flags))
+            assert np.array_equal(got, want)
+    finally:
+        t.close()
+
+
+def test_fetch_on_green_context_partition(dev):
+    """The same bytes when sampling + gather run on a green-context SM partition (step a6)."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+    c = gen.CONFIGS[1]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+        for flags in (dgz.PARTITION_SPREAD, dgz.PARTITION_FINE, 0):
+            part = dgz.Partition(8, -1, flags)
+            assert part.fetch_sms >= 8 and part.fetch_sms + part.compute_sms <= 148
+            f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, fetch_stream=part.fetch_stream)
+            for j in (0, 3):
+                seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
+                rs = gen.batch_rng_seed(c.seed, j)
+                mb = f.fetch(torch.from_numpy(seeds).pin_memory(), rs)
+                n = mb.sizes()[-1]
+                want = oracle.sample_uniform(off, col, seeds, c.fanouts, rs, with_blocks=False)
+                exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+                assert np.array_equal(mb.bufs.ids[:n].cpu().numpy(), want.U)
+                assert np.array_equal(mb.rows[:n].cpu().numpy(), exp)
+            del f
+            part.destroy()
+    finally:
+        t.close()
