@@ -253,24 +253,11 @@ def run_ours(args, d: Dist):
     fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True)
     cap = fetcher.bufs[0].bounds[-1]
     n_steps = torch.zeros(W + K, dtype=torch.int64, device="cuda")
-    s = fetcher.stream
     ceilings = measure_ceilings(dgz, info, R)
-    # per-step events on the fetch stream (torch.cuda.Event only sees the stream it is recorded on)
-    e_s = [ev() for _ in range(W + K)]
-    e_g = [ev() for _ in range(W + K)]
-    e_e = [ev() for _ in range(W + K)]
+    mbs = []
 
     def step(i):
-        p = i % 2
-        b = fetcher.bufs[p]
-        e_s[i].record(s)
-        with torch.cuda.stream(s):
-            dgz.sample_uniform(graph, seeds_dev[i], cfg.fanouts, rng[i], b, stream=s)
-            e_g[i].record(s)
-            dgz.gather_perm(table, b.ids_sorted, b.ids_sorted_pos, fetcher.rows[p], n=cap, n_dev=b.sizes_dev[L:L + 1],
-                            cfg=gcfg, stream=s)
-            e_e[i].record(s)
-            n_steps[i:i + 1].copy_(b.sizes_dev[L:L + 1], non_blocking=True)
+        mbs.append(fetcher.fetch(seeds_dev[i], rng[i], timing=True, count_into=n_steps[i:i + 1]))
 
     for i in range(W):
         step(i)
@@ -280,10 +267,11 @@ def run_ours(args, d: Dist):
     launches0 = dgz.kernel_launches()
     t_start, t_end = ev(), ev()
     with ClockSampler(d.local) as clk:
-        t_start.record(s)
+        t_start.record(fetcher.sample_stream)
         for i in range(W, W + K):
             step(i)
-        t_end.record(s)
+        fetcher.stream.wait_stream(fetcher.sample_stream)
+        t_end.record(fetcher.stream)
         torch.cuda.synchronize()
     launches = dgz.kernel_launches() - launches0
     d.barrier()
@@ -292,9 +280,10 @@ def run_ours(args, d: Dist):
     elapsed = t_start.elapsed_time(t_end) * 1e-3
     ns = n_steps.cpu().tolist()[W:]
     bytes_rank = float(sum(ns) * R)
-    gather_ms = [e_g[i].elapsed_time(e_e[i]) for i in range(W, W + K)]
-    sample_ms = [e_s[i].elapsed_time(e_g[i]) for i in range(W, W + K)]
-    step_ms = [e_s[i].elapsed_time(e_e[i]) for i in range(W, W + K)]
+    tm = [mbs[i].timing for i in range(W, W + K)]
+    gather_ms = [t[1].elapsed_time(t[2]) for t in tm]
+    sample_ms = [t[0].elapsed_time(t[1]) for t in tm]   # sample + wait for the previous gather
+    step_ms = [t[0].elapsed_time(t[2]) for t in tm]
     tot_bytes, = d.allreduce([bytes_rank], "sum")
     max_el, = d.allreduce([elapsed], "max")
     value = tot_bytes / max_el / 1e9
@@ -306,7 +295,7 @@ def run_ours(args, d: Dist):
     for i in (W + K - 2, W + K - 1):
         p = i % 2
         n = ns[i - W]
-        last[batches[i]] = (fetcher.bufs[p].ids[:n].cpu().numpy(), fetcher.rows[p][:n].cpu().numpy(), rng[i],
+        last[batches[i]] = (mbs[i].bufs.ids[:n].cpu().numpy(), mbs[i].rows[:n].cpu().numpy(), rng[i],
                             seeds_host[i].numpy())
 
     # ---- end-to-end through the public API: pinned host seeds -> H2D -> sample -> gather -> D2H |U|

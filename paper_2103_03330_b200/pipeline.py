@@ -24,8 +24,9 @@ class Minibatch:
     slot: int
     bufs: dgz.SampleBuffers
     rows: torch.Tensor          # [cap, row_bytes] uint8 in HBM: row r = table[ids[r]]
-    event: torch.cuda.Event     # recorded on the fetch stream after the gather
+    event: torch.cuda.Event     # recorded on the gather stream after the gather
     fanouts: tuple
+    timing: tuple | None = None  # (sample start, gather start, gather end) timing events
 
     @property
     def n_dev(self) -> torch.Tensor:
@@ -42,46 +43,77 @@ class Minibatch:
 
 
 class MinibatchFetcher:
-    """Owns ping-pong sample buffers and row buffers for one GPU and one registered table."""
+    """Owns ping-pong sample buffers and row buffers for one GPU and one registered table.
+
+    By default sampling and gather of a minibatch run back to back on one high-priority stream.
+    With ``overlap_sampling=True`` the sampler of minibatch j+1 runs on a second stream while the
+    gather of minibatch j runs (measured on B200: the sampler's full-GPU bitmap passes slow the
+    translation-bound gather more than the 0.36 ms they hide, so this is off by default).  Slot
+    reuse is ordered by events either way (a slot is resampled only after its gather and its
+    consumer are done).  An explicit ``fetch_stream`` (e.g. a green-context partition) is used
+    for both phases.
+    """
 
     def __init__(self, table: dgz.Table, graph: dgz.Graph, fanouts, max_seeds: int, slots: int = 2,
-                 gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None):
+                 gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None,
+                 overlap_sampling: bool = False):
         self.table, self.graph = table, graph
         self.fanouts = tuple(int(f) for f in fanouts)
         self.max_seeds = max_seeds
         self.cfg = gather_cfg
-        # high priority: the gather's few CTAs are scheduled ahead of the consumer's as SMs free up
-        self.stream = torch.cuda.Stream(priority=-1) if fetch_stream is None else fetch_stream
+        # high priority: the fetch's few CTAs are scheduled ahead of the consumer's as SMs free up
+        if fetch_stream is None:
+            self.stream = torch.cuda.Stream(priority=-1)
+            self.sample_stream = torch.cuda.Stream(priority=-1) if overlap_sampling else self.stream
+        else:
+            self.stream = self.sample_stream = fetch_stream
         self.bufs = [dgz.SampleBuffers(graph.n_nodes, max_seeds, self.fanouts, blocks=blocks, local=blocks,
                                        sorted_ids=True) for _ in range(slots)]
         cap = self.bufs[0].bounds[-1]
         self.rows = [torch.empty((cap, table.row_bytes), dtype=torch.uint8, device="cuda") for _ in range(slots)]
         self.seed_stage = [torch.empty(max_seeds, dtype=torch.int64, device="cuda") for _ in range(slots)]
-        self.events = [torch.cuda.Event() for _ in range(slots)]
-        self.free = [torch.cuda.Event() for _ in range(slots)]
+        self.events = [torch.cuda.Event() for _ in range(slots)]      # gather of slot p done
+        self.sampled = [torch.cuda.Event() for _ in range(slots)]     # sampling of slot p done
+        self.free = [torch.cuda.Event() for _ in range(slots)]        # consumer of slot p done
         self.next_slot = 0
 
     def release(self, mb: Minibatch, stream=None) -> None:
         """Mark slot `mb.slot` reusable once the consumer's queued work on `stream` is done."""
         self.free[mb.slot].record(torch.cuda.current_stream() if stream is None else stream)
 
-    def fetch(self, seeds: torch.Tensor, rng_seed: int, slot: int | None = None) -> Minibatch:
-        """Enqueue sampling + gather of one minibatch (seeds: int64, on the device or pinned host)."""
+    def fetch(self, seeds: torch.Tensor, rng_seed: int, slot: int | None = None, timing: bool = False,
+              count_into: torch.Tensor | None = None) -> Minibatch:
+        """Enqueue sampling + gather of one minibatch (seeds: int64, on the device or pinned host).
+        ``count_into``: a 1-element device int64 tensor that receives |U| on the gather stream."""
         p = self.next_slot if slot is None else slot
         self.next_slot = (p + 1) % len(self.bufs)
-        s = self.stream
-        s.wait_event(self.free[p])          # never overwrite rows the consumer still reads
+        ss, gs = self.sample_stream, self.stream
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+              torch.cuda.Event(enable_timing=True)) if timing else None
+        # slot p's sampler outputs and rows are free once its previous gather and consumer are done
+        ss.wait_event(self.events[p])
+        ss.wait_event(self.free[p])
         n_seeds = seeds.numel()
         assert n_seeds <= self.max_seeds
-        with torch.cuda.stream(s):
+        b = self.bufs[p]
+        L = len(self.fanouts)
+        with torch.cuda.stream(ss):
+            if ev:
+                ev[0].record(ss)
             if not seeds.is_cuda:
                 self.seed_stage[p][:n_seeds].copy_(seeds, non_blocking=True)   # H2D of the index list (P:552-553)
                 seeds = self.seed_stage[p][:n_seeds]
-            b = self.bufs[p]
-            dgz.sample_uniform(self.graph, seeds, self.fanouts, rng_seed, b, stream=s)
-            cap = b.bounds[-1]
-            L = len(self.fanouts)
-            dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=cap,
-                            n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=s)
-            self.events[p].record(s)
-        return Minibatch(p, b, self.rows[p], self.events[p], self.fanouts)
+            dgz.sample_uniform(self.graph, seeds, self.fanouts, rng_seed, b, stream=ss)
+            self.sampled[p].record(ss)
+        gs.wait_event(self.sampled[p])
+        with torch.cuda.stream(gs):
+            if ev:
+                ev[1].record(gs)
+            dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
+                            n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=gs)
+            if ev:
+                ev[2].record(gs)
+            if count_into is not None:
+                count_into.copy_(b.sizes_dev[L:L + 1], non_blocking=True)
+            self.events[p].record(gs)
+        return Minibatch(p, b, self.rows[p], self.events[p], self.fanouts, ev)
