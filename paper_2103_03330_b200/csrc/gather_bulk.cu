@@ -45,7 +45,7 @@ template <> struct piece_t<4> { using T = uint32_t; };
 template <> struct piece_t<2> { using T = uint16_t; };
 template <> struct piece_t<1> { using T = uint8_t; };
 
-// smem layout: [full mbarriers x S][empty mbarriers x S][slot metadata x S][pad][S slots]
+// smem layout: [full mbarriers x S][empty mbarriers x S][pad to 128 B][S slots]
 template <int SW, typename IdxT>
 __global__ void __launch_bounds__(1024, 1)
 gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
@@ -54,14 +54,14 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
-    int32_t* meta = reinterpret_cast<int32_t*>(empty + S);  // byte offset of the row in its slot, -1 = skip
-    uint8_t* slots = smem + (((size_t)S * 20 + 127) & ~size_t(127));
+    uint8_t* slots = smem + (((size_t)S * 16 + 127) & ~size_t(127));
 
     int64_t n = n_cap;
     if (n_dev) {
         const int64_t m = *n_dev;
         n = m < n_cap ? m : n_cap;
     }
+    const uint64_t base = reinterpret_cast<uint64_t>(src);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int nconsumers = nwarps - 1;
@@ -86,7 +86,6 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
         stride = gridDim.x;
         njobs = first < n ? (n - 1 - first) / stride + 1 : 0;
     }
-    const uint64_t base = reinterpret_cast<uint64_t>(src);
 
     if (warp == 0) {
         // producer warp: per round, lanes l < step issue jobs j0 + l (step <= S, so a slot is used
@@ -98,18 +97,21 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
             if (lane < step && j < njobs) {
                 const int s = (int)(j % S);
                 const int64_t use = j / S;
-                if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+                if (use > 0) {
+                    mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+                    // the consumers' generic-proxy reads of this slot precede the next async-proxy
+                    // (TMA) write into it
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
                 const int64_t r = first + j * stride;
                 const int64_t id = (int64_t)idx[r];
                 if (id < 0 || id >= rows) {
                     atomicOr(err, 1);
-                    meta[s] = -1;
                     mbar_arrive(&full[s]);
                 } else {
                     const uint64_t a = base + (uint64_t)id * (uint64_t)R;
                     const uint64_t a16 = a & ~uint64_t(15);
                     const uint32_t span = (uint32_t)(((a + (uint64_t)R + 15) & ~uint64_t(15)) - a16);
-                    meta[s] = (int32_t)(a - a16);
                     mbar_arrive_expect_tx(&full[s], span);
                     bulk_g2s(slots + (size_t)s * slot_bytes, a16, span, &full[s]);
                 }
@@ -120,11 +122,14 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
         using P = typename piece_t<SW>::T;
         for (int64_t j = warp - 1; j < njobs; j += nconsumers) {
             const int s = (int)(j % S);
+            const int64_t r = first + j * stride;
+            // the consumer re-derives the row's 16 B phase from its ID (no shared metadata:
+            // the only shared-memory traffic is the TMA-written slot, ordered by the mbarriers)
+            const int64_t id = (int64_t)idx[r];
             mbar_wait(&full[s], (uint32_t)((j / S) & 1));
-            const int off = meta[s];
-            if (off >= 0) {
+            if (id >= 0 && id < rows) {
+                const int off = (int)((base + (uint64_t)id * (uint64_t)R) & 15u);
                 const uint8_t* sp = slots + (size_t)s * slot_bytes + off;
-                const int64_t r = first + j * stride;
                 uint8_t* dp = dst + (dst_pos ? dst_pos[r] : r) * R;
                 for (int64_t q = (int64_t)lane * SW; q < R; q += 32 * SW)
                     *reinterpret_cast<P*>(dp + q) = *reinterpret_cast<const P*>(sp + q);
@@ -140,10 +145,10 @@ cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, const int64_t* ds
                         int* err, int blocks, int threads, int blocked, cudaStream_t s) {
     const int slot_bytes = (int)(((t->row_bytes + 32 + 127) / 128) * 128);
     const int max_smem = 227 * 1024;
-    int S = (max_smem - 256) / (slot_bytes + 20);
+    int S = (max_smem - 256) / (slot_bytes + 16);
     if (S > 1024) S = 1024;
     if (S < 2) return cudaErrorInvalidValue;
-    const size_t smem = (((size_t)S * 20 + 127) & ~size_t(127)) + (size_t)S * slot_bytes;
+    const size_t smem = (((size_t)S * 16 + 127) & ~size_t(127)) + (size_t)S * slot_bytes;
     cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<SW, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     gather_bulk_kernel<SW, IdxT><<<blocks, threads, smem, s>>>(t->dev, t->rows, t->row_bytes, idx, dst_pos, n, n_dev, out, err, S,
