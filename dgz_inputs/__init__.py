@@ -48,6 +48,7 @@ def lib() -> ctypes.CDLL:
         L.dgz_gen_batch_rng_seed.restype = u64
         L.dgz_gen_random_ids.argtypes = [i64, i64, u64, vp]
         L.dgz_gen_distinct_ids.argtypes = [i64, i64, u64, vp]
+        L.dgz_gen_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -57,6 +58,11 @@ def _ptr(a) -> int:
         assert a.flags["C_CONTIGUOUS"]
         return a.ctypes.data
     return int(a)
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the generators (results do not depend on it)."""
+    lib().dgz_gen_set_threads(int(n))
 
 
 # ----------------------------------------------------------------------------------------------

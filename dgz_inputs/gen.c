@@ -35,6 +35,15 @@ enum { ST_DEG = 1, ST_COL = 2, ST_TABLE = 3, ST_PERM = 4, ST_RNG = 5, ST_EPOCH =
 
 int dgz_gen_abi_version(void) { return 1; }
 
+/* Thread count of the OpenMP generators (torchrun sets OMP_NUM_THREADS=1 per rank). */
+void dgz_gen_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* Poisson(lambda) by inverse CDF with the pmf recursion, in double. lambda <= 700. */
 static int64_t poisson_inv(double lam, double u) {
     double p = exp(-lam), c = p;

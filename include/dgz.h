@@ -178,6 +178,16 @@ DGZ_API dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n,
 DGZ_API dgz_status dgz_gather_perm(dgz_table t, const int64_t* idx_dev, const int64_t* dst_pos_dev, int64_t n,
                                    const int64_t* n_dev, void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream);
 
+/* Address order of an arbitrary device ID list (duplicates allowed): ids_sorted[k] ascending and
+ * pos[k] its position in ids_dev -- the inputs of dgz_gather_perm, so that any gather can be
+ * fetched in table order (the sampler emits these for its own list).  IDs are compared on their
+ * low ceil(log2(max_id)) bits (pass max_id = table rows); out-of-range IDs still appear exactly
+ * once and are reported by the gather.  ids_sorted/pos: device int64 [n]; workspace: device
+ * scratch of dgz_order_workspace_bytes(n) bytes.  n < 2^31. */
+DGZ_API dgz_status dgz_order_workspace_bytes(int64_t n, size_t* bytes);
+DGZ_API dgz_status dgz_order_ids(const int64_t* ids_dev, int64_t n, int64_t max_id, int64_t* ids_sorted, int64_t* pos,
+                                 void* workspace, size_t workspace_bytes, dgz_stream stream);
+
 /* Synchronises `stream`, reads and clears the table's device RANGE flag for the current
  * device: DGZ_ERR_RANGE if any gather since the last check met an out-of-range ID. */
 DGZ_API dgz_status dgz_check_errors(dgz_table t, dgz_stream stream);

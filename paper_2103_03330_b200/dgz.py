@@ -97,6 +97,8 @@ _SIGS = {
     "dgz_gather_i32": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_gather_ex": ([_vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
     "dgz_gather_perm": ([_vp, _vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
+    "dgz_order_workspace_bytes": ([_i64, _P(_sz)], ctypes.c_int),
+    "dgz_order_ids": ([_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
     "dgz_check_errors": ([_vp, _vp], ctypes.c_int),
     "dgz_sample_bounds": ([_i64, _i64, _P(_i32), ctypes.c_int, _P(_i64), _P(_i64), _P(_i64)], ctypes.c_int),
     "dgz_sample_workspace_bytes": ([_i64, _i64, _P(_sz)], ctypes.c_int),
@@ -267,6 +269,20 @@ def gather_perm(table: Table, idx: torch.Tensor, dst_pos: torch.Tensor, out: tor
     _check(_lib.dgz_gather_perm(table.handle, _dptr(idx), _dptr(dst_pos), n, _dptr(n_dev), _dptr(out),
                                 ctypes.byref(cfg) if cfg is not None else None, _stream(stream)), "dgz_gather_perm")
     return out
+
+
+def order_ids(ids: torch.Tensor, max_id: int, stream=None) -> tuple:
+    """(ids_sorted, pos) for dgz_gather_perm (dgz_order_ids); allocates outputs and workspace."""
+    assert ids.dtype == torch.int64 and ids.is_cuda
+    n = ids.numel()
+    v = _sz()
+    _check(_lib.dgz_order_workspace_bytes(n, ctypes.byref(v)), "dgz_order_workspace_bytes")
+    ws = torch.empty(max(v.value, 1), dtype=torch.uint8, device=ids.device)
+    srt = torch.empty_like(ids)
+    pos = torch.empty_like(ids)
+    _check(_lib.dgz_order_ids(_dptr(ids), n, max_id, _dptr(srt), _dptr(pos), ws.data_ptr(), v.value, _stream(stream)),
+           "dgz_order_ids")
+    return srt, pos
 
 
 def check_errors(table: Table, stream=None) -> None:

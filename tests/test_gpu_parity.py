@@ -366,3 +366,34 @@ def test_fetch_on_green_context_partition(dev):
             part.destroy()
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("R,n", [(512, 5000), (100, 777), (2408, 3000), (64, 1)])
+def test_order_ids_then_gather_perm(dev, R, n):
+    """Arbitrary ID lists (duplicates, out of range) -> dgz_order_ids -> dgz_gather_perm."""
+    rows = 4000
+    t = HostTable(rows, R, seed=R + 5, dtype=dgz.F32)
+    try:
+        idx = gen.random_ids(rows, n, seed=n)
+        if n > 10:
+            idx[3] = idx[7]          # duplicate
+        ids = torch.from_numpy(idx).cuda()
+        srt, pos = dgz.order_ids(ids, rows)
+        torch.cuda.synchronize()
+        assert np.array_equal(srt.cpu().numpy(), np.sort(idx))
+        assert np.array_equal(idx[pos.cpu().numpy()], srt.cpu().numpy())
+        out = torch.empty(n * R, dtype=torch.uint8, device="cuda")
+        dgz.gather_perm(t.table, srt, pos, out)
+        torch.cuda.synchronize()
+        want, _ = oracle.gather(t.np, R, idx)
+        assert np.array_equal(out.cpu().numpy().reshape(n, R), want)
+        if n > 10:   # an out-of-range ID is kept once and reported by the gather
+            idx2 = idx.copy()
+            idx2[5] = rows + 3
+            srt, pos = dgz.order_ids(torch.from_numpy(idx2).cuda(), rows)
+            assert sorted(srt.cpu().tolist()) == sorted(idx2.tolist())
+            dgz.gather_perm(t.table, srt, pos, out)
+            with pytest.raises(dgz.RangeError):
+                dgz.check_errors(t.table)
+    finally:
+        t.close()
