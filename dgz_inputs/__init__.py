@@ -49,6 +49,7 @@ def lib() -> ctypes.CDLL:
         L.dgz_gen_random_ids.argtypes = [i64, i64, u64, vp]
         L.dgz_gen_distinct_ids.argtypes = [i64, i64, u64, vp]
         L.dgz_gen_set_threads.argtypes = [ctypes.c_int]
+        L.dgz_gen_cols32_skewed.argtypes = [i64, i64, u64, dbl, vp]
         _lib = L
     return _lib
 
@@ -69,14 +70,18 @@ def set_threads(n: int) -> None:
 # graph, table, seeds
 # ----------------------------------------------------------------------------------------------
 
-def gen_csr(n: int, avg_degree: float, seed: int, col_dtype=np.int32):
-    """CSR with Poisson(avg_degree) out-degrees and uniform endpoints."""
+def gen_csr(n: int, avg_degree: float, seed: int, col_dtype=np.int32, skew_alpha: float = 0.0):
+    """CSR with Poisson(avg_degree) out-degrees and uniform endpoints; with
+    skew_alpha > 1 the endpoints are power-law skewed (hot-row cache experiments, NEXT-1)."""
     off = np.empty(n + 1, dtype=np.int64)
     e = lib().dgz_gen_offsets(n, float(avg_degree), seed, _ptr(off))
     if e < 0:
         raise ValueError("bad graph parameters")
     col = np.empty(e, dtype=col_dtype)
-    if col_dtype == np.int32:
+    if skew_alpha > 1.0:
+        assert col_dtype == np.int32 and n < 2**31
+        lib().dgz_gen_cols32_skewed(n, e, seed, float(skew_alpha), _ptr(col))
+    elif col_dtype == np.int32:
         assert n < 2**31
         lib().dgz_gen_cols32(n, e, seed, _ptr(col))
     else:

@@ -146,3 +146,18 @@ void dgz_gen_distinct_ids(int64_t rows, int64_t n, uint64_t seed, int64_t* out) 
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) out[i] = (int64_t)feistel_perm((uint64_t)i, (uint64_t)rows, seed ^ 0xA5A5ull);
 }
+
+/* Skewed ("power-law") endpoints for the hot-row cache experiments:
+ * rank = floor(n * u^alpha) (alpha > 1 concentrates edges on low ranks: the top fraction x of
+ * ranks receives a share x^(1/alpha) of the edges), mapped to a node ID by a keyed permutation so
+ * that hot nodes are scattered over the table. */
+void dgz_gen_cols32_skewed(int64_t n, int64_t e_total, uint64_t seed, double alpha, int32_t* col) {
+    const uint64_t key = hk(seed, ST_PERM + 100, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < e_total; e++) {
+        double u = u01(hk(seed, ST_COL, (uint64_t)e));
+        int64_t r = (int64_t)((double)n * pow(u, alpha));
+        if (r >= n) r = n - 1;
+        col[e] = (int32_t)feistel_perm((uint64_t)r, (uint64_t)n, key);
+    }
+}

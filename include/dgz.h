@@ -98,6 +98,7 @@ DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 #define DGZ_REG_PORTABLE 1u  /* cudaHostRegisterPortable: valid on every device of this process */
 #define DGZ_REG_READONLY 2u  /* cudaHostRegisterReadOnly when the device supports it */
 #define DGZ_REG_NO_PIN 4u    /* memory is already page-locked (e.g. cudaHostAlloc): map only */
+#define DGZ_REG_DEVICE 16u    /* (reported) a device-resident table wrapped by dgz_wrap_device_table */
 #define DGZ_REG_VMM_BACKED 8u /* (reported in dgz_table_info.flags) the table lies in a DGZ_HOST_VMM
                                  allocation: no cudaHostRegister, large-page GPU mapping */
 
@@ -109,6 +110,10 @@ DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 DGZ_API dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int64_t dim, dgz_dtype dtype,
                               uint32_t flags, dgz_table* out);
 DGZ_API dgz_status dgz_unregister_table(dgz_table t);
+/* A handle for a table already resident in device memory (HBM), read by the same gather kernels:
+ * the paper's "All-in-GPU" reference point, and the source of cache shards.  The
+ * caller owns the memory; dgz_unregister_table releases only the handle. */
+DGZ_API dgz_status dgz_wrap_device_table(const void* dev_ptr, int64_t rows, int64_t dim, dgz_dtype dtype, dgz_table* out);
 
 typedef struct {
     const void* dev_ptr;     /* device-visible address of row 0 */
@@ -177,6 +182,34 @@ DGZ_API dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n,
  * DESIGN.md section 5).  dst_pos must be a permutation of [0, n) (else rows may overlap). */
 DGZ_API dgz_status dgz_gather_perm(dgz_table t, const int64_t* idx_dev, const int64_t* dst_pos_dev, int64_t n,
                                    const int64_t* n_dev, void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream);
+
+/* ==========================================================================================
+ * HBM row cache.  The paper found page-granular UVM caching "nearly
+ * useless" for irregular accesses; a ROW-granular cache of the most-referenced rows in
+ * HBM is a different design: on skewed graphs it removes their PCIe reads entirely.  The cache is
+ * a slot map (device int32 [rows], -1 = not cached) and G shards: slot s lives at row s / G of
+ * shard s % G.  Shards may be this GPU's HBM or peer GPUs' HBM mapped into this process (NVLink
+ * peer loads); all are caller-owned device memory of ceil(capacity / G) x row_bytes bytes.
+ * ========================================================================================== */
+#define DGZ_MAX_CACHE_SHARDS 8
+typedef struct {
+    int32_t* slot_map;    /* device int32 [table rows] */
+    int32_t n_shards;     /* 1 <= G <= DGZ_MAX_CACHE_SHARDS */
+    int32_t reserved;
+    void* shards[DGZ_MAX_CACHE_SHARDS];
+} dgz_cache_view;
+
+/* Build: slot_map[hot_ids[c]] = c for c < n_hot, every other entry -1, and shard (c % G) row
+ * (c / G) = table row hot_ids[c] (fetched by zero-copy).  hot_ids: device int64 [n_hot], distinct
+ * and in range (DGZ_ERR_RANGE is latched in the table flag otherwise).  One-time setup: may
+ * allocate temporary device memory. */
+DGZ_API dgz_status dgz_cache_fill(dgz_table t, const int64_t* hot_ids_dev, int64_t n_hot, const dgz_cache_view* cache,
+                                  dgz_stream stream);
+/* As dgz_gather_perm (dst_pos_dev may be NULL: identity), reading cached rows from HBM and the
+ * others by zero-copy from the table: out[dst_pos[k]] = table[idx[k]] either way (byte-exact). */
+DGZ_API dgz_status dgz_gather_cached(dgz_table t, const dgz_cache_view* cache, const int64_t* idx_dev,
+                                     const int64_t* dst_pos_dev, int64_t n, const int64_t* n_dev, void* out_dev,
+                                     const dgz_gather_cfg* cfg, dgz_stream stream);
 
 /* Address order of an arbitrary device ID list (duplicates allowed): ids_sorted[k] ascending and
  * pos[k] its position in ids_dev -- the inputs of dgz_gather_perm, so that any gather can be

@@ -239,6 +239,25 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
     return DGZ_OK;
 }
 
+extern "C" dgz_status dgz_wrap_device_table(const void* dev_ptr, int64_t rows, int64_t dim, dgz_dtype dtype, dgz_table* out) {
+    DGZ_REQUIRE(out && dev_ptr && rows >= 1 && dim >= 1, "dgz_wrap_device_table: bad arguments");
+    *out = nullptr;
+    const int eb = elem_bytes_of(dtype);
+    DGZ_REQUIRE(eb > 0 && ((uintptr_t)dev_ptr % eb) == 0, "dgz_wrap_device_table: bad dtype or alignment");
+    dgz_table t = new (std::nothrow) dgz_table_s();
+    if (!t) { set_error("out of memory"); return DGZ_ERR_NOMEM; }
+    t->host = t->dev = (const uint8_t*)dev_ptr;
+    t->rows = rows;
+    t->dim = dim;
+    t->elem_bytes = eb;
+    t->row_bytes = dim * eb;
+    t->flags = DGZ_REG_NO_PIN | DGZ_REG_DEVICE;
+    cudaError_t e = cudaGetDevice(&t->device);
+    if (e != cudaSuccess) { delete t; return cuda_fail(e, "cudaGetDevice"); }
+    *out = t;
+    return DGZ_OK;
+}
+
 extern "C" dgz_status dgz_unregister_table(dgz_table t) {
     DGZ_REQUIRE(t, "dgz_unregister_table: null table");
     dgz_status st = DGZ_OK;

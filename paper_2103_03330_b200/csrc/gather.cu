@@ -85,11 +85,19 @@ __device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo,
     }
 }
 
-template <int SW, int U, bool HINT, typename IdxT>
+// HBM row cache: slot[id] >= 0 -> the row lives in shard (slot % G) at
+// row (slot / G) (local HBM, or a peer GPU's HBM mapped into this address space).
+struct CacheArgs {
+    const int32_t* slot;
+    int32_t G;
+    const uint8_t* shard[DGZ_MAX_CACHE_SHARDS];
+};
+
+template <int SW, int U, bool HINT, bool CACHED, typename IdxT>
 __global__ void __launch_bounds__(512, 1)
 gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
                       const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
-                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked) {
+                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked, const CacheArgs ca) {
     int64_t n = n_cap;
     if (n_dev) {
         const int64_t m = *n_dev;
@@ -121,31 +129,45 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
         bstep = int64_t(gridDim.x) * wpc;
     }
 
-    // software-pipelined ID load: the next batch's ID is fetched before this batch's PCIe loads
-    int64_t id_next = -1, dp_next = -1;
-    if (bcur < bend && (bcur << 5) + lane < n) {
-        id_next = (int64_t)idx[(bcur << 5) + lane];
-        dp_next = dst_pos ? dst_pos[(bcur << 5) + lane] : (bcur << 5) + lane;
-    }
+    // Software-pipelined index loads: IDs two batches ahead, the cache slot (which depends on the
+    // ID) one batch ahead, the destination row one batch ahead -- none of them stalls the PCIe
+    // loads of the current batch.
+    auto load_id = [&](int64_t bb) -> int64_t {
+        const int64_t rr = (bb << 5) + lane;
+        return (bb < bend && rr < n) ? (int64_t)idx[rr] : -1;
+    };
+    auto load_dp = [&](int64_t bb) -> int64_t {
+        const int64_t rr = (bb << 5) + lane;
+        return (bb < bend && rr < n) ? (dst_pos ? dst_pos[rr] : rr) : -1;
+    };
+    auto load_slot = [&](int64_t id) -> int32_t {
+        if constexpr (CACHED) return (id >= 0 && id < rows) ? ca.slot[id] : -1;
+        return -1;
+    };
+    int64_t id_n1 = load_id(bcur), id_n2 = load_id(bcur + bstep);
+    int64_t dp_n1 = load_dp(bcur);
+    int32_t sl_n1 = load_slot(id_n1);
 
     for (; bcur < bend; bcur += bstep) {
         const int64_t b0 = bcur << 5;
         const int64_t r = b0 + lane;
-        int64_t id = id_next;
-        const int64_t drow = dp_next;
-        {
-            const int64_t bn = bcur + bstep;
-            const int64_t rn = (bn << 5) + lane;
-            const bool ok = bn < bend && rn < n;
-            id_next = ok ? (int64_t)idx[rn] : -1;
-            dp_next = ok ? (dst_pos ? dst_pos[rn] : rn) : -1;
-        }
+        int64_t id = id_n1;
+        const int64_t drow = dp_n1;
+        const int32_t slot = sl_n1;
+        id_n1 = id_n2;
+        sl_n1 = load_slot(id_n1);
+        dp_n1 = load_dp(bcur + bstep);
+        id_n2 = load_id(bcur + 2 * bstep);
         if (r < n && (id < 0 || id >= rows)) {
             atomicOr(err, 1);
             id = -1;
         }
         if (r >= n) id = -1;
-        const uint64_t a = base + (uint64_t)(id < 0 ? 0 : id) * (uint64_t)R;
+        uint64_t a = base + (uint64_t)(id < 0 ? 0 : id) * (uint64_t)R;
+        if constexpr (CACHED) {
+            if (id >= 0 && slot >= 0)
+                a = reinterpret_cast<uint64_t>(ca.shard[slot % ca.G]) + (uint64_t)(slot / ca.G) * (uint64_t)R;
+        }
         const uint64_t l0 = a & ~uint64_t(127);
         const int nl = id < 0 ? 0 : (int)((a + (uint64_t)R - l0 + 127) >> 7);
         int incl = nl;
@@ -236,6 +258,7 @@ gather_elem_kernel(const T* __restrict__ src, int64_t rows, int64_t F, const Idx
 }
 
 struct SegLaunch {
+    const CacheArgs* cache;
     int flags;
     const int64_t* dst_pos;
     int64_t n;
@@ -248,8 +271,13 @@ struct SegLaunch {
 
 template <int SW, int U, bool HINT, typename IdxT>
 void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
-    gather_segment_kernel<SW, U, HINT, IdxT><<<L.blocks, L.threads, 0, L.s>>>(t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n,
-                                                                              L.n_dev, L.out, L.err, L.blocked);
+    if (L.cache) {
+        gather_segment_kernel<SW, U, HINT, true, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
+            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache);
+    } else {
+        gather_segment_kernel<SW, U, HINT, false, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
+            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, CacheArgs{});
+    }
     dgz::count_launch();
 }
 
@@ -305,7 +333,7 @@ dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, 
                            const int64_t* n_dev, void* out, int* err, int sms, int warps, int blocked, cudaStream_t s);
 
 dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n, const int64_t* n_dev,
-                           void* out, const dgz_gather_cfg* cfg, cudaStream_t s) {
+                           void* out, const dgz_gather_cfg* cfg, cudaStream_t s, const dgz_cache_view* cache) {
     DGZ_REQUIRE(t, "dgz_gather: null table");
     DGZ_REQUIRE(n >= 0, "dgz_gather: n < 0");
     if (n == 0) return DGZ_OK;
@@ -335,13 +363,14 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     // local and still covers the PCIe bandwidth-delay product; it also leaves SMs free.
     const bool sorted_path = dst_pos != nullptr;
     int k = bounded ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : nsm;
+    const bool hbm_table = t->flags & DGZ_REG_DEVICE;   // HBM-resident: latency-bound, wants many warps
     int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta
-                                                : (variant == DGZ_GATHER_BULK ? 8 : (sorted_path ? 2 : 16));
+                                                : (variant == DGZ_GATHER_BULK ? 8 : ((sorted_path && !hbm_table) ? 2 : 16));
     int flags = cfg ? cfg->flags : 0;
-    if (sorted_path && !bounded && !(cfg && cfg->warps_per_cta > 0) && flags == 0) flags = DGZ_GATHER_FLAG_DEEP;
+    if (sorted_path && !hbm_table && !bounded && !(cfg && cfg->warps_per_cta > 0) && flags == 0) flags = DGZ_GATHER_FLAG_DEEP;
     const int max_warps = variant == DGZ_GATHER_SEGMENT ? 16 : 32;  // SEGMENT: <= 512 threads (128 regs)
     if (warps > max_warps) warps = max_warps;
-    int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : 1;
+    int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : (hbm_table ? 4 : 1);
     if (warps * cps > 64) cps = 64 / warps > 0 ? 64 / warps : 1;
     const int sched = cfg ? cfg->schedule : DGZ_SCHED_AUTO;
     const int blocked = sched == DGZ_SCHED_BLOCKED;
@@ -355,9 +384,21 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
         int64_t blocks = (int64_t)k * cps;
         int64_t need = (batches + warps - 1) / warps;
         if (blocks > need) blocks = need;
-        const uint64_t x = (uint64_t)t->row_bytes | ((uint64_t)(uintptr_t)t->dev & 15u) | ((uint64_t)(uintptr_t)out & 15u) | 16u;
+        uint64_t x = (uint64_t)t->row_bytes | ((uint64_t)(uintptr_t)t->dev & 15u) | ((uint64_t)(uintptr_t)out & 15u) | 16u;
+        CacheArgs ca{};
+        if (cache) {
+            DGZ_REQUIRE(cache->slot_map && cache->n_shards >= 1 && cache->n_shards <= DGZ_MAX_CACHE_SHARDS,
+                        "dgz_gather_cached: bad cache view");
+            ca.slot = cache->slot_map;
+            ca.G = cache->n_shards;
+            for (int g = 0; g < ca.G; ++g) {
+                DGZ_REQUIRE(cache->shards[g], "dgz_gather_cached: null shard %d", g);
+                ca.shard[g] = (const uint8_t*)cache->shards[g];
+                x |= (uint64_t)(uintptr_t)cache->shards[g] & 15u;   // stores must suit every source base
+            }
+        }
         const int sw = (int)(x & (~x + 1));
-        SegLaunch L{flags, dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s};
+        SegLaunch L{cache ? &ca : nullptr, flags, dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s};
         if (idx_is64)
             e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, L);
         else
@@ -382,20 +423,28 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
 }
 
 extern "C" dgz_status dgz_gather(dgz_table t, const int64_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
-    return dgz_gather_impl(t, idx_dev, 1, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 1, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream, nullptr);
 }
 
 extern "C" dgz_status dgz_gather_i32(dgz_table t, const int32_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
-    return dgz_gather_impl(t, idx_dev, 0, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 0, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream, nullptr);
 }
 
 extern "C" dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n, const int64_t* n_dev, void* out_dev,
                                     const dgz_gather_cfg* cfg, dgz_stream stream) {
-    return dgz_gather_impl(t, idx_dev, 1, nullptr, n, n_dev, out_dev, cfg, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 1, nullptr, n, n_dev, out_dev, cfg, (cudaStream_t)stream, nullptr);
 }
 
 extern "C" dgz_status dgz_gather_perm(dgz_table t, const int64_t* idx_dev, const int64_t* dst_pos_dev, int64_t n,
                                       const int64_t* n_dev, void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream) {
     DGZ_REQUIRE(dst_pos_dev || n == 0, "dgz_gather_perm: null dst_pos");
-    return dgz_gather_impl(t, idx_dev, 1, dst_pos_dev, n, n_dev, out_dev, cfg, (cudaStream_t)stream);
+    return dgz_gather_impl(t, idx_dev, 1, dst_pos_dev, n, n_dev, out_dev, cfg, (cudaStream_t)stream, nullptr);
+}
+
+extern "C" dgz_status dgz_gather_cached(dgz_table t, const dgz_cache_view* cache, const int64_t* idx_dev, const int64_t* dst_pos_dev,
+                                        int64_t n, const int64_t* n_dev, void* out_dev, const dgz_gather_cfg* cfg, dgz_stream stream) {
+    DGZ_REQUIRE(cache, "dgz_gather_cached: null cache view");
+    DGZ_REQUIRE(!cfg || cfg->variant == DGZ_GATHER_AUTO || cfg->variant == DGZ_GATHER_SEGMENT,
+                "dgz_gather_cached: only the SEGMENT variant reads the cache");
+    return dgz_gather_impl(t, idx_dev, 1, dst_pos_dev, n, n_dev, out_dev, cfg, (cudaStream_t)stream, cache);
 }

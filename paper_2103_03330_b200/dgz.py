@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(_SO)
 # --- constants (dgz.h) -------------------------------------------------------------------------
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_RANGE, ERR_STATE = range(6)
 F32, F16, BF16, U8 = range(4)
-REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED = 1, 2, 4, 8
+REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED, REG_DEVICE = 1, 2, 4, 8, 16
 HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM, HOST_CUDA_PINNED, HOST_HUGETLB_2M, HOST_HUGETLB_1G = 1, 2, 4, 8, 16, 32
 GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
 SCHED_AUTO, SCHED_INTERLEAVED, SCHED_BLOCKED = range(3)
@@ -63,6 +63,14 @@ class GatherCfg(ctypes.Structure):
                 ("ctas_per_sm", ctypes.c_int32), ("schedule", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
 
+MAX_CACHE_SHARDS = 8
+
+
+class CacheView(ctypes.Structure):
+    _fields_ = [("slot_map", ctypes.c_void_p), ("n_shards", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("shards", ctypes.c_void_p * MAX_CACHE_SHARDS)]
+
+
 class Csr(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int64), ("offsets", ctypes.c_void_p), ("cols", ctypes.c_void_p),
                 ("cols_is64", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -92,6 +100,9 @@ _SIGS = {
     "dgz_host_import": ([ctypes.c_int, _sz, _P(_vp)], ctypes.c_int),
     "dgz_register_table": ([_vp, _i64, _i64, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
     "dgz_unregister_table": ([_vp], ctypes.c_int),
+    "dgz_wrap_device_table": ([_vp, _i64, _i64, ctypes.c_int, _P(_vp)], ctypes.c_int),
+    "dgz_cache_fill": ([_vp, _vp, _i64, _P(CacheView), _vp], ctypes.c_int),
+    "dgz_gather_cached": ([_vp, _P(CacheView), _vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
     "dgz_table_get_info": ([_vp, _P(TableInfo)], ctypes.c_int),
     "dgz_gather": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_gather_i32": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
@@ -230,6 +241,46 @@ class Table:
 
 def register_table(host_ptr: int, rows: int, dim: int, dtype: int = F32, flags: int = 0) -> Table:
     return Table(host_ptr, rows, dim, dtype, flags)
+
+
+class DeviceTable(Table):
+    """A table resident in HBM (dgz_wrap_device_table): the All-in-GPU reference."""
+
+    def __init__(self, dev_ptr: int, rows: int, dim: int, dtype: int = F32):
+        h = _vp()
+        _check(_lib.dgz_wrap_device_table(dev_ptr, rows, dim, dtype, ctypes.byref(h)), "dgz_wrap_device_table")
+        self.handle = h.value
+        self.dtype = dtype
+        self.info = self.get_info()
+
+
+class HotRowCache:
+    """Row-granular HBM cache of a registered table (dgz_cache_fill / dgz_gather_cached).
+    Shards are local device memory here; peer-mapped shards use the same view (NVLink loads)."""
+
+    def __init__(self, table: Table, hot_ids: torch.Tensor, n_shards: int = 1, stream=None):
+        assert hot_ids.dtype == torch.int64 and hot_ids.is_cuda and 1 <= n_shards <= MAX_CACHE_SHARDS
+        self.table = table
+        n_hot = hot_ids.numel()
+        per = (n_hot + n_shards - 1) // n_shards
+        self.slot_map = torch.empty(table.rows, dtype=torch.int32, device=hot_ids.device)
+        self.shards = [torch.empty((max(per, 1), table.row_bytes), dtype=torch.uint8, device=hot_ids.device)
+                       for _ in range(n_shards)]
+        self.view = CacheView(self.slot_map.data_ptr(), n_shards, 0)
+        for g, sh in enumerate(self.shards):
+            self.view.shards[g] = sh.data_ptr()
+        self.n_hot = n_hot
+        _check(_lib.dgz_cache_fill(table.handle, _dptr(hot_ids) if n_hot else None, n_hot, ctypes.byref(self.view),
+                                   _stream(stream)), "dgz_cache_fill")
+
+    def gather(self, idx: torch.Tensor, out: torch.Tensor, dst_pos: torch.Tensor | None = None, n: int | None = None,
+               n_dev: torch.Tensor | None = None, cfg: GatherCfg | None = None, stream=None) -> torch.Tensor:
+        n = idx.numel() if n is None else n
+        assert idx.dtype == torch.int64
+        _check(_lib.dgz_gather_cached(self.table.handle, ctypes.byref(self.view), _dptr(idx), _dptr(dst_pos), n,
+                                      _dptr(n_dev), _dptr(out), ctypes.byref(cfg) if cfg is not None else None,
+                                      _stream(stream)), "dgz_gather_cached")
+        return out
 
 
 def unregister_table(t: Table) -> None:

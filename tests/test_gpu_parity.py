@@ -397,3 +397,59 @@ def test_order_ids_then_gather_perm(dev, R, n):
                 dgz.check_errors(t.table)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+@pytest.mark.parametrize("R,base", [(512, 0), (400, 16), (2408, 8), (100, 4)])
+def test_hot_row_cache_gather(dev, G, R, base):
+    """NEXT-1 HBM row cache: cached rows from HBM shards, the rest by zero-copy; same bytes."""
+    rows = 5000
+    t = HostTable(rows, R, seed=R + G, base=base, dtype=dgz.F32)
+    try:
+        hot = gen.distinct_ids(rows, 700, seed=G)
+        cache = dgz.HotRowCache(t.table, torch.from_numpy(hot).cuda(), n_shards=G)
+        torch.cuda.synchronize()
+        dgz.check_errors(t.table)
+        sm = cache.slot_map.cpu().numpy()
+        assert (sm[hot] == np.arange(700)).all() and (np.delete(sm, hot) == -1).all()
+        for g in range(G):   # shard g row k = table[hot[g + k*G]]
+            k = np.arange(g, 700, G)
+            want, _ = oracle.gather(t.np, R, hot[k])
+            assert np.array_equal(cache.shards[g][:k.shape[0]].cpu().numpy(), want)
+        idx = np.concatenate([gen.random_ids(rows, 2000, seed=R), hot[:300]])
+        want, _ = oracle.gather(t.np, R, idx)
+        out = torch.full((idx.shape[0] * R,), 0xAB, dtype=torch.uint8, device="cuda")
+        cache.gather(torch.from_numpy(idx).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+        o = np.argsort(idx, kind="stable")
+        out.fill_(0xAB)
+        cache.gather(torch.from_numpy(idx[o]).cuda(), out, dst_pos=torch.from_numpy(o.astype(np.int64)).cuda(),
+                     cfg=dgz.gather_cfg(sm_count=5, warps_per_cta=2))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+    finally:
+        t.close()
+
+
+def test_device_table_and_empty_cache(dev):
+    R, rows = 512, 3000
+    t = HostTable(rows, R, seed=11, dtype=dgz.F32)
+    try:
+        dev_copy = torch.from_numpy(t.np.copy()).cuda()
+        dt = dgz.DeviceTable(dev_copy.data_ptr(), rows, R // 4, dgz.F32)
+        assert dt.info.flags & dgz.REG_DEVICE
+        idx = gen.random_ids(rows, 1000, seed=2)
+        want, _ = oracle.gather(t.np, R, idx)
+        out = torch.empty(1000 * R, dtype=torch.uint8, device="cuda")
+        dgz.gather(dt, torch.from_numpy(idx).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+        dt.unregister()
+        cache = dgz.HotRowCache(t.table, torch.zeros(0, dtype=torch.int64, device="cuda"))
+        out.zero_()
+        cache.gather(torch.from_numpy(idx).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+    finally:
+        t.close()
