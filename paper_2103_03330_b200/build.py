@@ -65,6 +65,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, SO)
+    # a plain C program against the C ABI (examples/c_abi_gather.c): proves the boundary needs
+    # nothing but include/dgz.h, libdgz.so and the CUDA runtime
+    ex_src = os.path.join(ROOT, "examples", "c_abi_gather.c")
+    ex_bin = os.path.join(ROOT, "examples", "c_abi_gather")
+    if os.path.exists(ex_src) and (force or _stale([ex_src, SO, os.path.join(INC, "dgz.h")], ex_bin)):
+        cmd = ["gcc", "-O2", "-std=c11", "-I", INC, "-I", "/usr/local/cuda/include", ex_src, "-o", ex_bin,
+               "-L", PKG, "-ldgz", "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,$ORIGIN/../paper_2103_03330_b200",
+               "-Wl,-rpath,/usr/local/cuda/lib64"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
         print("\n".join(logs))
     return SO
