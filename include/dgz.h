@@ -86,8 +86,9 @@ DGZ_API dgz_status dgz_host_unlink(const char* shm_name);
  * pass it to another process (SCM_RIGHTS / pidfd_getfd) and map it there with dgz_host_import.
  * The caller closes the fd. */
 DGZ_API dgz_status dgz_host_export(void* ptr, int* fd);
-/* Map an exported DGZ_HOST_VMM allocation of `bytes` bytes into this process, accessible by the
- * CPU and the current device.  Release with dgz_host_free. */
+/* Map an exported DGZ_HOST_VMM allocation into this process, accessible by the CPU and the current
+ * device.  `bytes` must be the size the exporter passed to dgz_host_alloc (the whole allocation is
+ * mapped).  Release with dgz_host_free. */
 DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 
 /* ==========================================================================================

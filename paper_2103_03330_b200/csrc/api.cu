@@ -54,6 +54,7 @@ using namespace dgz;
 
 static std::mutex g_pinned_mu;
 static std::map<uintptr_t, size_t> g_pinned;  // cudaHostAlloc'ed host tables -> bytes
+static std::map<uintptr_t, size_t> g_mapped;  // hugetlb mappings -> mapped (rounded) bytes
 
 dgz_status dgz_vmm_alloc(size_t bytes, void** ptr);
 int dgz_vmm_free(void* ptr);
@@ -87,9 +88,15 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
     void* p = MAP_FAILED;
     if (!shm_name) {
         int extra = 0;
-        if (flags & DGZ_HOST_HUGETLB_2M) extra = MAP_HUGETLB | (21 << MAP_HUGE_SHIFT);
-        if (flags & DGZ_HOST_HUGETLB_1G) extra = MAP_HUGETLB | (30 << MAP_HUGE_SHIFT);
-        p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | extra, -1, 0);
+        size_t huge = 0;
+        if (flags & DGZ_HOST_HUGETLB_2M) { extra = MAP_HUGETLB | (21 << MAP_HUGE_SHIFT); huge = size_t(1) << 21; }
+        if (flags & DGZ_HOST_HUGETLB_1G) { extra = MAP_HUGETLB | (30 << MAP_HUGE_SHIFT); huge = size_t(1) << 30; }
+        const size_t mapped = huge ? (bytes + huge - 1) / huge * huge : bytes;   // munmap needs the huge-page multiple
+        p = mmap(nullptr, mapped, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | extra, -1, 0);
+        if (p != MAP_FAILED && huge) {
+            std::lock_guard<std::mutex> g(g_pinned_mu);
+            g_mapped[(uintptr_t)p] = mapped;
+        }
     } else {
         DGZ_REQUIRE(shm_name[0] == '/', "dgz_host_alloc: shm name must start with '/'");
         int fd = shm_open(shm_name, O_RDWR | (create ? O_CREAT : 0), 0600);
@@ -131,6 +138,14 @@ extern "C" dgz_status dgz_host_free(void* ptr, size_t bytes) {
             cudaError_t e = cudaFreeHost(ptr);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFreeHost");
             return DGZ_OK;
+        }
+    }
+    {
+        std::lock_guard<std::mutex> g(g_pinned_mu);
+        auto it = g_mapped.find((uintptr_t)ptr);
+        if (it != g_mapped.end()) {
+            bytes = it->second;
+            g_mapped.erase(it);
         }
     }
     if (munmap(ptr, bytes) != 0) { set_error("munmap: %s", strerror(errno)); return DGZ_ERR_INVALID; }

@@ -453,3 +453,32 @@ def test_device_table_and_empty_cache(dev):
         assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
     finally:
         t.close()
+
+
+def test_host_allocation_kinds(dev):
+    """Every host-table allocation kind registers and gathers the same bytes; VMM export/import
+    maps the same pages at a second address."""
+    import os as _os
+    R, rows = 512, 4096
+    nbytes = R * rows
+    idx = gen.random_ids(rows, 700, seed=5)
+    kinds = [("anon", dgz.HOST_HUGEPAGE), ("cudapin", dgz.HOST_CUDA_PINNED), ("vmm", dgz.HOST_VMM)]
+    for name, flags in kinds:
+        buf = dgz.HostBuffer(nbytes, flags=flags)
+        host = buf.numpy(0, nbytes)
+        gen.fill_table(buf.ptr, nbytes, 17)
+        t = dgz.register_table(buf.ptr, rows, R // 4, dgz.F32)
+        want, _ = oracle.gather(host, R, idx)
+        out = torch.empty(700 * R, dtype=torch.uint8, device="cuda")
+        dgz.gather(t.table if hasattr(t, "table") else t, torch.from_numpy(idx).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want), name
+        if name == "vmm":
+            assert t.info.flags & dgz.REG_VMM_BACKED
+            fd = buf.export_fd()
+            b2 = dgz.HostBuffer(nbytes, import_fd=fd)
+            assert b2.ptr != buf.ptr and np.array_equal(b2.numpy(0, 4096), host[:4096])
+            b2.free()
+            _os.close(fd)
+        t.unregister()
+        buf.free()
