@@ -141,6 +141,9 @@ DGZ_API dgz_status dgz_table_get_info(dgz_table t, dgz_table_info* info);
  * output bytes are left unchanged) and the table's RANGE flag is latched (dgz_check_errors).
  * ========================================================================================== */
 DGZ_API dgz_status dgz_gather(dgz_table t, const int64_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream);
+/* (dgz_gather on a host table of >= 4 GiB with n >= 65536 rows fetches in table-address order --
+ * device radix sort + dgz_gather_perm, scratch from cudaMallocAsync -- because GPU address
+ * translation of 4 KiB host pages bounds random rows there; the result is identical.) */
 DGZ_API dgz_status dgz_gather_i32(dgz_table t, const int32_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream);
 
 typedef enum {
@@ -169,6 +172,8 @@ typedef struct {
 } dgz_gather_cfg;
 #define DGZ_GATHER_FLAG_L2_EVICT_FIRST 1 /* zero-copy loads with an L2 evict-first cache policy */
 #define DGZ_GATHER_FLAG_DEEP 2           /* 16 instead of 8 line loads in flight per lane */
+#define DGZ_GATHER_FLAG_ORDER 4          /* dgz_gather_ex: fetch in table-address order (sort on the
+                                            device, gather, scatter back); same result */
 
 /* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
  * gathers min(*n_dev, n) rows (n is the capacity), so a gather can follow the sampler on the

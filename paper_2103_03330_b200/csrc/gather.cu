@@ -422,7 +422,37 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     return DGZ_OK;
 }
 
+extern "C" dgz_status dgz_order_workspace_bytes(int64_t n, size_t* bytes);
+extern "C" dgz_status dgz_order_ids(const int64_t* ids_dev, int64_t n, int64_t max_id, int64_t* ids_sorted, int64_t* pos,
+                                    void* workspace, size_t workspace_bytes, dgz_stream stream);
+
+// Fetch in table order: sort (id, position) on the device, gather in address order and scatter
+// back (GPU address translation of 4 KiB host pages bounds random rows on
+// large tables).  Scratch comes from the stream-ordered allocator (pooled, non-blocking).
+static dgz_status gather_ordered(dgz_table t, const int64_t* idx, int64_t n, void* out, const dgz_gather_cfg* cfg,
+                                 cudaStream_t s) {
+    size_t ws = 0;
+    dgz_status st = dgz_order_workspace_bytes(n, &ws);
+    if (st != DGZ_OK) return st;
+    const size_t arr = ((size_t)n * 8 + 255) & ~size_t(255);
+    uint8_t* mem = nullptr;
+    DGZ_CUDA(cudaMallocAsync((void**)&mem, 2 * arr + ws, s));
+    int64_t* srt = (int64_t*)mem;
+    int64_t* pos = (int64_t*)(mem + arr);
+    st = dgz_order_ids(idx, n, t->rows, srt, pos, mem + 2 * arr, ws, (dgz_stream)s);
+    if (st == DGZ_OK) st = dgz_gather_impl(t, srt, 1, pos, n, nullptr, out, cfg, s, nullptr);
+    cudaFreeAsync(mem, s);
+    return st;
+}
+
+static bool want_order(const dgz_table_s* t, int64_t n) {
+    // large host tables only: below a few GiB the GPU's translation caches cover the table
+    return !(t->flags & DGZ_REG_DEVICE) && n >= (int64_t(1) << 16) && n < (int64_t(1) << 31) &&
+           (double)t->rows * (double)t->row_bytes >= 4.0 * (1 << 30);
+}
+
 extern "C" dgz_status dgz_gather(dgz_table t, const int64_t* idx_dev, int64_t n, void* out_dev, dgz_stream stream) {
+    if (t && idx_dev && out_dev && want_order(t, n)) return gather_ordered(t, idx_dev, n, out_dev, nullptr, (cudaStream_t)stream);
     return dgz_gather_impl(t, idx_dev, 1, nullptr, n, nullptr, out_dev, nullptr, (cudaStream_t)stream, nullptr);
 }
 
@@ -432,6 +462,16 @@ extern "C" dgz_status dgz_gather_i32(dgz_table t, const int32_t* idx_dev, int64_
 
 extern "C" dgz_status dgz_gather_ex(dgz_table t, const int64_t* idx_dev, int64_t n, const int64_t* n_dev, void* out_dev,
                                     const dgz_gather_cfg* cfg, dgz_stream stream) {
+    if (cfg && (cfg->flags & DGZ_GATHER_FLAG_ORDER)) {
+        DGZ_REQUIRE(t && idx_dev && out_dev && !n_dev && n >= 0 && n < (int64_t(1) << 31),
+                    "dgz_gather_ex: DGZ_GATHER_FLAG_ORDER needs a host-known n < 2^31 and no n_dev");
+        DGZ_REQUIRE(cfg->variant == DGZ_GATHER_AUTO || cfg->variant == DGZ_GATHER_SEGMENT || cfg->variant == DGZ_GATHER_BULK,
+                    "dgz_gather_ex: DGZ_GATHER_FLAG_ORDER needs the SEGMENT or BULK variant");
+        if (n == 0) return DGZ_OK;
+        dgz_gather_cfg c2 = *cfg;
+        c2.flags &= ~DGZ_GATHER_FLAG_ORDER;
+        return gather_ordered(t, idx_dev, n, out_dev, &c2, (cudaStream_t)stream);
+    }
     return dgz_gather_impl(t, idx_dev, 1, nullptr, n, n_dev, out_dev, cfg, (cudaStream_t)stream, nullptr);
 }
 

@@ -41,6 +41,14 @@ def test_full_size_config(cid):
             exp = np.empty(n * R, dtype=np.uint8)
             assert oracle.gather_into(host.ctypes.data, c.n_nodes, R, want.U, exp) == 0
             assert np.array_equal(mb.rows[:n].cpu().numpy().reshape(-1), exp)
+        if c.table_bytes >= 4 << 30:
+            # plain dgz_gather of a large unsorted list: fetched in address order internally
+            idx = gen.random_ids(c.n_nodes, 100_000, seed=3)
+            out = torch.empty(100_000 * R, dtype=torch.uint8, device="cuda")
+            dgz.gather(table, torch.from_numpy(idx).cuda(), out)
+            exp = np.empty(100_000 * R, dtype=np.uint8)
+            oracle.gather_into(host.ctypes.data, c.n_nodes, R, idx, exp)
+            assert np.array_equal(out.cpu().numpy(), exp)
         dgz.check_errors(table)
     finally:
         table.unregister()

@@ -482,3 +482,24 @@ def test_host_allocation_kinds(dev):
             _os.close(fd)
         t.unregister()
         buf.free()
+
+
+@pytest.mark.parametrize("variant", [1, 4])
+def test_gather_flag_order(dev, variant):
+    """DGZ_GATHER_FLAG_ORDER: sort on the device, gather in address order, scatter back."""
+    R, rows = 400, 6000
+    t = HostTable(rows, R, seed=21, base=16, dtype=dgz.F32)
+    try:
+        idx = gen.random_ids(rows, 5000, seed=4)
+        idx[10] = idx[20]
+        want, _ = oracle.gather(t.np, R, idx)
+        got = _gather_dev(t, idx, cfg=dgz.gather_cfg(variant=variant, flags=dgz.FLAG_ORDER))
+        assert np.array_equal(got, want)
+        bad = idx.copy()
+        bad[7] = rows + 1
+        got = _gather_dev(t, bad, cfg=dgz.gather_cfg(variant=variant, flags=dgz.FLAG_ORDER))
+        with pytest.raises(dgz.RangeError):
+            dgz.check_errors(t.table)
+        assert (got[7] == 0xAB).all() and np.array_equal(got[8:], want[8:])
+    finally:
+        t.close()
