@@ -327,6 +327,10 @@ DGZ_API dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32_t 
 /* Dependent-load chain of `steps` hops through a mapped host array of int64 "next" offsets;
  * writes cycles_dev[0] = total cycles, cycles_dev[1] = final offset (one thread;
  * RTT = cycles / steps / SM clock).  cycles_dev: device uint64 [2]. */
+/* Pure-ALU load (dependent FMA chains, no memory traffic): `ctas` x `threads` threads spin for
+ * `iters` iterations.  Used to separate SM-issue from memory-system interference in the overlap
+ * experiments.  sink_dev: device float [1]. */
+DGZ_API dgz_status dgz_probe_spin(int32_t ctas, int32_t threads, int64_t iters, float* sink_dev, dgz_stream stream);
 DGZ_API dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream);
 
 #ifdef __cplusplus

@@ -44,9 +44,26 @@ __global__ void chase_kernel(const int64_t* __restrict__ src, int64_t steps, uin
     cycles[1] = (uint64_t)p;
 }
 
+// pure-ALU load: dependent FMA chains, no memory traffic (interference experiments)
+__global__ void spin_kernel(int64_t iters, float* sink) {
+    float a = threadIdx.x * 1e-3f, b = 1.0001f, c = 0.9999f;
+    for (int64_t i = 0; i < iters; ++i) {
+        a = fmaf(a, b, c);
+        b = fmaf(b, c, a * 1e-9f);
+    }
+    if (a == 1234.5f) sink[0] = b;
+}
+
 }  // namespace
 
 using namespace dgz;
+
+extern "C" dgz_status dgz_probe_spin(int32_t ctas, int32_t threads, int64_t iters, float* sink_dev, dgz_stream stream) {
+    DGZ_REQUIRE(ctas > 0 && threads > 0 && threads <= 1024 && iters >= 0 && sink_dev, "dgz_probe_spin: bad args");
+    spin_kernel<<<ctas, threads, 0, (cudaStream_t)stream>>>(iters, sink_dev);
+    dgz::count_launch();
+    return launch_check("spin_kernel");
+}
 
 extern "C" dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32_t sm_count, int32_t warps, int32_t unroll,
                                        uint64_t* sink_dev, dgz_stream stream) {

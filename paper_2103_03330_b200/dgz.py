@@ -121,6 +121,7 @@ _SIGS = {
     "dgz_partition_destroy": ([_vp], ctypes.c_int),
     "dgz_probe_stream": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
+    "dgz_probe_spin": ([_i32, _i32, _i64, _vp, _vp], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -461,3 +462,7 @@ def probe_stream(src_dev_ptr: int, nbytes: int, sm_count: int, warps: int, unrol
 
 def probe_chase(src_dev_ptr: int, steps: int, cycles: torch.Tensor, stream=None):
     _check(_lib.dgz_probe_chase(src_dev_ptr, steps, _dptr(cycles), _stream(stream)), "dgz_probe_chase")
+
+
+def probe_spin(ctas: int, threads: int, iters: int, sink: torch.Tensor, stream=None):
+    _check(_lib.dgz_probe_spin(ctas, threads, iters, _dptr(sink), _stream(stream)), "dgz_probe_spin")
