@@ -6,9 +6,10 @@
 //          F_{k+1} = F_k ++ sorted(unique(selected) \ F_k)            (readings R9-R10)
 //
 // B200 design: the frontier set F_k is a bitmap over all N nodes in HBM (N/8 bytes: 14 MB for
-// the papers100M-shaped graph).  Selected IDs are OR-ed into a candidate bitmap; one pass over
-// the two bitmaps (popcount per 4096-word chunk, a single-block scan, an emit pass) yields the
-// new IDs already sorted and de-duplicated, with no sort and no hash table.  Every size that
+// the papers100M-shaped graph).  Selected IDs are OR-ed into a candidate bitmap; ONE single-pass
+// compaction over the two bitmaps (per 4096-word chunk: popcount, decoupled look-back for the
+// chunk's prefix, emit) yields the new IDs already sorted and de-duplicated, with no sort and no
+// hash table.  A minibatch is 1 + 2L (+1 sorted, +1 local positions) kernel launches.  Every size that
 // depends on the data (|F_k|) stays on the device: kernels read it from sizes_dev, so the whole
 // minibatch (sampling + gather) is enqueued without a host round trip and can be graph-captured.
 #include <cub/block/block_reduce.cuh>
@@ -93,24 +94,6 @@ hop_sample_kernel(const int64_t* __restrict__ off, const ColT* __restrict__ cols
     }
 }
 
-// popcount of (cand & ~front) per chunk
-__global__ void __launch_bounds__(kChunkThreads)
-bitmap_count_kernel(const uint32_t* __restrict__ front, const uint32_t* __restrict__ cand, int64_t* __restrict__ chunk_sums) {
-    using BR = cub::BlockReduce<int, kChunkThreads>;
-    __shared__ typename BR::TempStorage tmp;
-    const int64_t w0 = int64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
-    int c = 0;
-    const uint4* cf = reinterpret_cast<const uint4*>(front + w0);
-    const uint4* cc = reinterpret_cast<const uint4*>(cand + w0);
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread / 4; ++q) {
-        const uint4 a = cc[q], b = cf[q];
-        c += __popc(a.x & ~b.x) + __popc(a.y & ~b.y) + __popc(a.z & ~b.z) + __popc(a.w & ~b.w);
-    }
-    const int tot = BR(tmp).Sum(c);
-    if (threadIdx.x == 0) chunk_sums[blockIdx.x] = tot;
-}
-
 // exclusive scan of chunk sums (one block); *total_out = (base ? *base : 0) + sum
 __global__ void __launch_bounds__(1024)
 scan_chunks_kernel(const int64_t* __restrict__ sums, int64_t nchunks, int64_t* __restrict__ offs, const int64_t* base,
@@ -131,87 +114,6 @@ scan_chunks_kernel(const int64_t* __restrict__ sums, int64_t nchunks, int64_t* _
         __syncthreads();
     }
     if (threadIdx.x == 0) *total_out = (base ? *base : 0) + carry;
-}
-
-// emit the new IDs (cand & ~front) in ascending order at U[sizes[k] + ...]; front |= cand; cand = 0
-__global__ void __launch_bounds__(kChunkThreads)
-bitmap_emit_kernel(uint32_t* __restrict__ front, uint32_t* __restrict__ cand, const int64_t* __restrict__ chunk_offs,
-                   const int64_t* __restrict__ sizes, int k, int64_t* __restrict__ U) {
-    using BS = cub::BlockScan<int, kChunkThreads>;
-    __shared__ typename BS::TempStorage tmp;
-    const int64_t w0 = int64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
-    uint32_t nw[kWordsPerThread];
-    int c = 0;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        const uint32_t a = cand[w0 + q], b = front[w0 + q];
-        nw[q] = a & ~b;
-        c += __popc(nw[q]);
-        if (a) {
-            front[w0 + q] = a | b;
-            cand[w0 + q] = 0;
-        }
-    }
-    int ex;
-    BS(tmp).ExclusiveSum(c, ex);
-    if (!c) return;
-    int64_t p = sizes[k] + chunk_offs[blockIdx.x] + ex;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        uint32_t bits = nw[q];
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            U[p++] = (w0 + q) * 32 + b;
-            bits &= bits - 1;
-        }
-    }
-}
-
-// ---- U in ascending order (the final frontier bitmap) with each ID's position in U ----------
-__global__ void __launch_bounds__(kChunkThreads)
-bitmap_count_all_kernel(const uint32_t* __restrict__ front, int64_t* __restrict__ chunk_sums) {
-    using BR = cub::BlockReduce<int, kChunkThreads>;
-    __shared__ typename BR::TempStorage tmp;
-    const int64_t w0 = int64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
-    const uint4* cf = reinterpret_cast<const uint4*>(front + w0);
-    int c = 0;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread / 4; ++q) {
-        const uint4 b = cf[q];
-        c += __popc(b.x) + __popc(b.y) + __popc(b.z) + __popc(b.w);
-    }
-    const int tot = BR(tmp).Sum(c);
-    if (threadIdx.x == 0) chunk_sums[blockIdx.x] = tot;
-}
-__global__ void __launch_bounds__(kChunkThreads)
-bitmap_emit_sorted_kernel(const uint32_t* __restrict__ front, const int64_t* __restrict__ chunk_offs, const int32_t* __restrict__ pos,
-                          int64_t* __restrict__ sorted, int64_t* __restrict__ sorted_pos) {
-    using BS = cub::BlockScan<int, kChunkThreads>;
-    __shared__ typename BS::TempStorage tmp;
-    const int64_t w0 = int64_t(blockIdx.x) * kChunkWords + threadIdx.x * kWordsPerThread;
-    uint32_t w[kWordsPerThread];
-    int c = 0;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        w[q] = front[w0 + q];
-        c += __popc(w[q]);
-    }
-    int ex;
-    BS(tmp).ExclusiveSum(c, ex);
-    if (!c) return;
-    int64_t p = chunk_offs[blockIdx.x] + ex;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        uint32_t bits = w[q];
-        while (bits) {
-            const int b = __ffs(bits) - 1;
-            const int64_t id = (w0 + q) * 32 + b;
-            sorted[p] = id;
-            sorted_pos[p] = pos[id];
-            ++p;
-            bits &= bits - 1;
-        }
-    }
 }
 
 // ---- seeds: F_0 = seeds with the first occurrence of each ID kept -----------------------------
@@ -266,23 +168,157 @@ seeds_emit_kernel(const int64_t* __restrict__ seeds, int64_t n, int64_t N, const
     }
 }
 
-__global__ void posmap_kernel(const int64_t* __restrict__ U, const int64_t* __restrict__ sizes, int L, int32_t* __restrict__ pos) {
-    const int64_t n = sizes[L];
+// ---- fused single-pass compaction (decoupled look-back) ---------------------------------------
+// One launch per hop instead of count + scan + emit: each 4096-word chunk takes a ticket (so a
+// chunk only ever waits for chunks that already started), publishes its popcount, looks back
+// over its predecessors' published aggregates / inclusive prefixes, and emits its IDs in order.
+// MODE_NEW: the new IDs of hop k (cand & ~front) are appended to U at sizes[k] + prefix, their
+//           positions recorded in pos[], front |= cand, cand = 0; the last chunk writes sizes[k+1].
+// MODE_ALL: all IDs of the final frontier in ascending order with their positions in U.
+constexpr int MODE_NEW = 0, MODE_ALL = 1;
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+template <int MODE>
+__global__ void __launch_bounds__(kChunkThreads)
+bitmap_compact_kernel(uint32_t* __restrict__ front, uint32_t* __restrict__ cand, unsigned long long* __restrict__ status,
+                      unsigned* __restrict__ ticket, int64_t nchunks, int64_t* __restrict__ sizes, int k, int64_t* __restrict__ U,
+                      int32_t* __restrict__ pos, int64_t* __restrict__ sorted, int64_t* __restrict__ sorted_pos) {
+    using BS = cub::BlockScan<int, kChunkThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ int chunk_s;
+    __shared__ long long prefix_s;
+    if (threadIdx.x == 0) chunk_s = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int chunk = chunk_s;
+    const int64_t w0 = int64_t(chunk) * kChunkWords + threadIdx.x * kWordsPerThread;
+    uint32_t nw[kWordsPerThread];
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        if (MODE == MODE_NEW) {
+            const uint32_t a = cand[w0 + q], b = front[w0 + q];
+            nw[q] = a & ~b;
+            if (a) {
+                front[w0 + q] = a | b;
+                cand[w0 + q] = 0;
+            }
+        } else {
+            nw[q] = front[w0 + q];
+        }
+        c += __popc(nw[q]);
+    }
+    int ex, agg;
+    BS(tmp).ExclusiveSum(c, ex, agg);
+    if (threadIdx.x == 0) {
+        long long prefix = 0;
+        if (chunk == 0) {
+            atomicExch(&status[0], kFlagIncl | (unsigned long long)agg);
+        } else {
+            atomicExch(&status[chunk], kFlagAgg | (unsigned long long)agg);
+            for (int j = chunk - 1; j >= 0;) {
+                const unsigned long long v = atomicAdd(&status[j], 0ull);
+                const unsigned long long flag = v & ~kValMask;
+                if (flag == 0) continue;  // predecessor started (ticket order) but not published yet
+                prefix += (long long)(v & kValMask);
+                if (flag == kFlagIncl) break;
+                --j;
+            }
+            atomicExch(&status[chunk], kFlagIncl | (unsigned long long)(prefix + agg));
+        }
+        prefix_s = prefix;
+        if (MODE == MODE_NEW && chunk == nchunks - 1) sizes[k + 1] = sizes[k] + prefix + agg;
+    }
+    __syncthreads();
+    if (!c) return;
+    int64_t p = (MODE == MODE_NEW ? sizes[k] : 0) + prefix_s + ex;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        uint32_t bits = nw[q];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            const int64_t id = (w0 + q) * 32 + b;
+            if (MODE == MODE_NEW) {
+                U[p] = id;
+                pos[id] = (int32_t)p;
+            } else {
+                sorted[p] = id;
+                sorted_pos[p] = pos[id];
+            }
+            ++p;
+            bits &= bits - 1;
+        }
+    }
+}
+
+// F_0 for up to kSmallSeeds seeds in one block: first occurrence kept, positions recorded
+constexpr int kSmallSeeds = 8192;
+__global__ void __launch_bounds__(1024)
+seeds_small_kernel(const int64_t* __restrict__ seeds, int n, int64_t N, int64_t* __restrict__ U, uint32_t* __restrict__ front,
+                   int32_t* __restrict__ pos, int64_t* __restrict__ sizes, int* __restrict__ err) {
+    extern __shared__ int64_t sh[];
+    using BS = cub::BlockScan<int, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ int run;
+    for (int i = threadIdx.x; i < n; i += 1024) {
+        const int64_t v = seeds[i];
+        const bool ok = v >= 0 && v < N;
+        if (!ok) atomicOr(err, 1);
+        sh[i] = ok ? v : -1;
+    }
+    if (threadIdx.x == 0) run = 0;
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += 1024) {
+        const int i = i0 + threadIdx.x;
+        bool keep = false;
+        if (i < n && sh[i] >= 0) {
+            keep = true;
+            const int64_t v = sh[i];
+            for (int j = 0; j < i; ++j)
+                if (sh[j] == v) { keep = false; break; }
+        }
+        int ex, agg;
+        BS(tmp).ExclusiveSum((int)keep, ex, agg);
+        if (keep) {
+            const int64_t v = sh[i];
+            const int p = run + ex;
+            U[p] = v;
+            pos[v] = p;
+            atomicOr(&front[v >> 5], 1u << (v & 31));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) run += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sizes[0] = run;
+}
+
+__global__ void posmap_range_kernel(const int64_t* __restrict__ U, const int64_t* __restrict__ sizes, int32_t* __restrict__ pos) {
+    const int64_t n = sizes[0];
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) pos[U[i]] = (int32_t)i;
 }
-__global__ void local_kernel(const int64_t* __restrict__ nbr, const int64_t* __restrict__ sizes, int k, int f,
-                             const int32_t* __restrict__ pos, int32_t* __restrict__ local) {
-    const int64_t n = sizes[k] * f;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t s = nbr[i];
-        local[i] = s < 0 ? -1 : pos[s];
+
+// positions in U of every sampled ID, all hops in one launch
+struct HopTable {
+    int64_t start[DGZ_MAX_LAYERS + 1];  // element offset of hop k's block (bound-based layout)
+    int32_t f[DGZ_MAX_LAYERS];
+    int32_t L;
+};
+__global__ void local_all_kernel(const int64_t* __restrict__ nbr, const int64_t* __restrict__ sizes, const HopTable ht,
+                                 const int32_t* __restrict__ pos, int32_t* __restrict__ local) {
+    const int64_t total = ht.start[ht.L];
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        int k = 0;
+        while (k + 1 < ht.L && e >= ht.start[k + 1]) ++k;
+        if (ht.f[k] == 0 || e - ht.start[k] >= sizes[k] * ht.f[k]) continue;  // beyond this hop's |F_k|
+        const int64_t v = nbr[e];
+        local[e] = v < 0 ? -1 : pos[v];
     }
 }
 
 // ---- workspace layout ----------------------------------------------------------------------
 struct Layout {
     int64_t nwords_pad, nchunks, seed_chunks;
-    size_t o_front, o_cand, o_csum, o_coff, o_ssum, o_soff, o_pos, o_err, total;
+    size_t o_front, o_cand, o_status, o_ticket, o_zero_end, o_csum, o_coff, o_ssum, o_soff, o_pos, o_err, total;
 };
 inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 Layout layout(int64_t N, int64_t max_seeds) {
@@ -296,6 +332,9 @@ Layout layout(int64_t N, int64_t max_seeds) {
     l.o_err = o; o = al(o + 8);  // first: dgz_sample_check finds it without the layout
     l.o_front = o; o = al(o + 4 * (size_t)l.nwords_pad);
     l.o_cand = o; o = al(o + 4 * (size_t)l.nwords_pad);
+    l.o_status = o; o = al(o + 8 * (size_t)l.nchunks * (DGZ_MAX_LAYERS + 1));   // one look-back array per compaction
+    l.o_ticket = o; o = al(o + 4 * (DGZ_MAX_LAYERS + 1));
+    l.o_zero_end = o;                                                            // everything above is zeroed per call
     l.o_csum = o; o = al(o + 8 * ((size_t)l.nchunks + 1));
     l.o_coff = o; o = al(o + 8 * (size_t)l.nchunks);
     l.o_ssum = o; o = al(o + 8 * (size_t)l.seed_chunks);
@@ -382,9 +421,15 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
     int* err = (int*)(ws + l.o_err);
     int64_t* sizes = out->sizes_dev;
 
-    DGZ_CUDA(cudaMemsetAsync(ws, 0, l.o_csum, s));  // error word + both bitmaps
-    // F_0
-    if (n_seeds > 0) {
+    unsigned long long* status = (unsigned long long*)(ws + l.o_status);
+    unsigned* tickets = (unsigned*)(ws + l.o_ticket);
+    DGZ_CUDA(cudaMemsetAsync(ws, 0, l.o_zero_end, s));  // error word, bitmaps, look-back state
+    // F_0 (pos[] of every ID of U is written where the ID is emitted)
+    if (n_seeds > 0 && n_seeds <= kSmallSeeds) {
+        seeds_small_kernel<<<1, 1024, sizeof(int64_t) * (size_t)n_seeds, s>>>(seeds_dev, (int)n_seeds, N, out->ids, front, pos, sizes,
+                                                                            err);
+        dgz::count_launch();
+    } else if (n_seeds > 0) {
         const int gs = grid_for(n_seeds, 256);
         const int sc = (int)((n_seeds + kSeedChunk - 1) / kSeedChunk);
         seeds_mark_kernel<<<gs, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, err); dgz::count_launch();
@@ -392,11 +437,14 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
         seeds_count_kernel<<<sc, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, ssum); dgz::count_launch();
         scan_chunks_kernel<<<1, 1024, 0, s>>>(ssum, sc, soff, nullptr, sizes); dgz::count_launch();
         seeds_emit_kernel<<<sc, 256, 0, s>>>(seeds_dev, n_seeds, N, pos, soff, out->ids, front); dgz::count_launch();
+        posmap_range_kernel<<<gs, 256, 0, s>>>(out->ids, sizes, pos); dgz::count_launch();
     } else {
         DGZ_CUDA(cudaMemsetAsync(sizes, 0, 8, s));
     }
     int64_t nbr_off = 0, cnt_off = 0;
     const uint32_t k0 = (uint32_t)(rng_seed & 0xffffffffu), k1 = (uint32_t)(rng_seed >> 32);
+    HopTable ht{};
+    ht.L = n_layers;
     for (int k = 0; k < n_layers; ++k) {
         const int f = fanouts[k];
         int64_t* nbr_k = out->nbr ? out->nbr + nbr_off : nullptr;
@@ -409,32 +457,25 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
             hop_sample_kernel<int32_t><<<gh, 256, 0, s>>>(csr->offsets, (const int32_t*)csr->cols, out->ids, sizes, k, f, k0, k1, nbr_k,
                                                           cnt_k, cand);
         dgz::count_launch();
-        bitmap_count_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, cand, csum); dgz::count_launch();
-        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, sizes + k, sizes + k + 1); dgz::count_launch();
-        bitmap_emit_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, cand, coff, sizes, k, out->ids); dgz::count_launch();
+        bitmap_compact_kernel<MODE_NEW><<<(int)l.nchunks, kChunkThreads, 0, s>>>(
+            front, cand, status + (size_t)k * l.nchunks, tickets + k, l.nchunks, sizes, k, out->ids, pos, nullptr, nullptr);
+        dgz::count_launch();
+        ht.start[k] = nbr_off;
+        ht.f[k] = f;
         nbr_off += bounds[k] * f;
         cnt_off += bounds[k];
     }
-    if (out->nbr_local || out->ids_sorted) {
-        posmap_kernel<<<grid_for(bounds[n_layers], 256), 256, 0, s>>>(out->ids, sizes, n_layers, pos);
-        dgz::count_launch();
-    }
+    ht.start[n_layers] = nbr_off;
     if (out->ids_sorted) {
         // the final frontier bitmap holds exactly U: compact it in ascending ID order
-        bitmap_count_all_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, csum); dgz::count_launch();
-        scan_chunks_kernel<<<1, 1024, 0, s>>>(csum, l.nchunks, coff, nullptr, csum + l.nchunks); dgz::count_launch();
-        bitmap_emit_sorted_kernel<<<(int)l.nchunks, kChunkThreads, 0, s>>>(front, coff, pos, out->ids_sorted, out->ids_sorted_pos); dgz::count_launch();
+        bitmap_compact_kernel<MODE_ALL><<<(int)l.nchunks, kChunkThreads, 0, s>>>(
+            front, cand, status + (size_t)n_layers * l.nchunks, tickets + n_layers, l.nchunks, sizes, n_layers, nullptr, pos,
+            out->ids_sorted, out->ids_sorted_pos);
+        dgz::count_launch();
     }
-    if (out->nbr_local) {
-        int64_t o = 0;
-        for (int k = 0; k < n_layers; ++k) {
-            if (fanouts[k] > 0) {
-                local_kernel<<<grid_for(bounds[k] * fanouts[k], 256), 256, 0, s>>>(out->nbr + o, sizes, k, fanouts[k], pos,
-                                                                                 out->nbr_local + o);
-                dgz::count_launch();
-            }
-            o += bounds[k] * fanouts[k];
-        }
+    if (out->nbr_local && nbr_off > 0) {
+        local_all_kernel<<<grid_for(nbr_off, 256), 256, 0, s>>>(out->nbr, sizes, ht, pos, out->nbr_local);
+        dgz::count_launch();
     }
     st = launch_check("dgz_sample_uniform kernels");
     if (st != DGZ_OK) return st;
