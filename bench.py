@@ -254,7 +254,7 @@ def run_ours(args, d: Dist):
     gcfg = dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps) if (args.gather_sms or args.gather_warps) else None
     sm_count_all = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True,
-                               sampler_sms=args.sampler_sms)
+                               sampler_sms=args.sampler_sms, graphs=args.graphs)
     cap = fetcher.bufs[0].bounds[-1]
     n_steps = torch.zeros(W + K, dtype=torch.int64, device="cuda")
     ceilings = measure_ceilings(dgz, info, R)
@@ -617,6 +617,7 @@ def main():
     ap.add_argument("--gather-warps", type=int, default=0)
     ap.add_argument("--sampler-sms", type=int, default=8,
                     help="SMs of the green-context sampler partition (0 = sample and gather back to back)")
+    ap.add_argument("--graphs", action="store_true", help="replay sampler + gather as one CUDA graph per slot")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false")
     args = ap.parse_args()

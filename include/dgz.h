@@ -268,6 +268,9 @@ typedef struct {
     int64_t* ids_sorted;   /* optional device [ids_cap]: the IDs of `ids` in ascending order */
     int64_t* ids_sorted_pos; /* optional device [ids_cap] (with ids_sorted): position in `ids` of
                               each sorted ID -- the inputs of dgz_gather_perm */
+    const uint64_t* rng_seed_dev; /* optional device uint64 [1]: when set, the sampler reads its
+                              seed here and ignores `rng_seed` (a captured CUDA graph can then be
+                              replayed for a new minibatch by updating seeds and this word) */
 } dgz_sample_out;
 
 /* bounds[k] = min(n_nodes, n_seeds * prod_{i<k}(1 + fanouts[i])) for k = 0..L; also the

@@ -48,9 +48,15 @@ __device__ __forceinline__ uint32_t philox4x32_10_w0(uint32_t c0, uint32_t c1, u
 template <typename ColT>
 __global__ void __launch_bounds__(256)
 hop_sample_kernel(const int64_t* __restrict__ off, const ColT* __restrict__ cols, const int64_t* __restrict__ U,
-                  const int64_t* __restrict__ sizes, int k, int f, uint32_t key0, uint32_t key1, int64_t* __restrict__ nbr,
-                  int32_t* __restrict__ cnt, uint32_t* __restrict__ cand) {
+                  const int64_t* __restrict__ sizes, int k, int f, uint32_t key0, uint32_t key1,
+                  const uint64_t* __restrict__ key_dev, int64_t* __restrict__ nbr, int32_t* __restrict__ cnt,
+                  uint32_t* __restrict__ cand) {
     const int64_t nk = sizes[k];
+    if (key_dev) {  // device-resident sampler seed (CUDA-graph replays update it in place)
+        const uint64_t kk = *key_dev;
+        key0 = (uint32_t)(kk & 0xffffffffu);
+        key1 = (uint32_t)(kk >> 32);
+    }
     uint32_t pos[DGZ_MAX_FANOUT];
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nk; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t u = U[i];
@@ -184,59 +190,76 @@ bitmap_compact_kernel(uint32_t* __restrict__ front, uint32_t* __restrict__ cand,
                       unsigned* __restrict__ ticket, int64_t nchunks, int64_t* __restrict__ sizes, int k, int64_t* __restrict__ U,
                       int32_t* __restrict__ pos, int64_t* __restrict__ sorted, int64_t* __restrict__ sorted_pos) {
     using BS = cub::BlockScan<int, kChunkThreads>;
-    __shared__ typename BS::TempStorage tmp;
+    using BR = cub::BlockReduce<int, kChunkThreads>;
+    __shared__ union {
+        typename BS::TempStorage scan;
+        typename BR::TempStorage reduce;
+    } tmp;
     __shared__ int chunk_s;
     __shared__ long long prefix_s;
     if (threadIdx.x == 0) chunk_s = (int)atomicAdd(ticket, 1u);
     __syncthreads();
     const int chunk = chunk_s;
-    const int64_t w0 = int64_t(chunk) * kChunkWords + threadIdx.x * kWordsPerThread;
+    // word r*256 + t of the chunk goes to thread t: coalesced loads, and the IDs of a sparse or
+    // dense region are spread over all threads when they are emitted
+    const int64_t wbase = int64_t(chunk) * kChunkWords + threadIdx.x;
     uint32_t nw[kWordsPerThread];
     int c = 0;
 #pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
+    for (int r = 0; r < kWordsPerThread; ++r) {
+        const int64_t w = wbase + r * kChunkThreads;
         if (MODE == MODE_NEW) {
-            const uint32_t a = cand[w0 + q], b = front[w0 + q];
-            nw[q] = a & ~b;
+            const uint32_t a = cand[w], b = front[w];
+            nw[r] = a & ~b;
             if (a) {
-                front[w0 + q] = a | b;
-                cand[w0 + q] = 0;
+                front[w] = a | b;
+                cand[w] = 0;
             }
         } else {
-            nw[q] = front[w0 + q];
+            nw[r] = front[w];
         }
-        c += __popc(nw[q]);
+        c += __popc(nw[r]);
     }
-    int ex, agg;
-    BS(tmp).ExclusiveSum(c, ex, agg);
-    if (threadIdx.x == 0) {
+    const int agg_t0 = BR(tmp.reduce).Sum(c);   // valid in thread 0
+    if (threadIdx.x < 32) {
+        // warp-parallel decoupled look-back: 32 predecessors per step, newest first
+        const int lane = threadIdx.x;
+        const int agg = __shfl_sync(0xffffffffu, agg_t0, 0);
+        if (lane == 0) atomicExch(&status[chunk], (chunk == 0 ? kFlagIncl : kFlagAgg) | (unsigned long long)agg);
         long long prefix = 0;
-        if (chunk == 0) {
-            atomicExch(&status[0], kFlagIncl | (unsigned long long)agg);
-        } else {
-            atomicExch(&status[chunk], kFlagAgg | (unsigned long long)agg);
-            for (int j = chunk - 1; j >= 0;) {
-                const unsigned long long v = atomicAdd(&status[j], 0ull);
-                const unsigned long long flag = v & ~kValMask;
-                if (flag == 0) continue;  // predecessor started (ticket order) but not published yet
-                prefix += (long long)(v & kValMask);
-                if (flag == kFlagIncl) break;
-                --j;
+        for (int j_hi = chunk - 1; j_hi >= 0; j_hi -= 32) {
+            const int j = j_hi - lane;
+            unsigned long long v = j >= 0 ? atomicAdd(&status[j], 0ull) : kFlagIncl;
+            while (__any_sync(0xffffffffu, (v & ~kValMask) == 0)) {   // started (ticket order), not yet published
+                if ((v & ~kValMask) == 0) v = atomicAdd(&status[j], 0ull);
             }
-            atomicExch(&status[chunk], kFlagIncl | (unsigned long long)(prefix + agg));
+            const unsigned incl = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagIncl);
+            const int stop = incl ? __ffs(incl) - 1 : 31;                // newest inclusive prefix ends the walk
+            long long val = lane <= stop ? (long long)(v & kValMask) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) val += __shfl_down_sync(0xffffffffu, val, o);
+            prefix += __shfl_sync(0xffffffffu, val, 0);
+            if (incl) break;
         }
-        prefix_s = prefix;
-        if (MODE == MODE_NEW && chunk == nchunks - 1) sizes[k + 1] = sizes[k] + prefix + agg;
+        if (lane == 0) {
+            if (chunk > 0) atomicExch(&status[chunk], kFlagIncl | (unsigned long long)(prefix + agg));
+            prefix_s = prefix;
+            if (MODE == MODE_NEW && chunk == nchunks - 1) sizes[k + 1] = sizes[k] + prefix + agg;
+        }
     }
     __syncthreads();
-    if (!c) return;
-    int64_t p = (MODE == MODE_NEW ? sizes[k] : 0) + prefix_s + ex;
+    int64_t run = (MODE == MODE_NEW ? sizes[k] : 0) + prefix_s;
 #pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        uint32_t bits = nw[q];
+    for (int r = 0; r < kWordsPerThread; ++r) {
+        const int cnt = __popc(nw[r]);
+        int ex, ragg;
+        BS(tmp.scan).ExclusiveSum(cnt, ex, ragg);
+        int64_t p = run + ex;
+        uint32_t bits = nw[r];
+        const int64_t w = wbase + r * kChunkThreads;
         while (bits) {
             const int b = __ffs(bits) - 1;
-            const int64_t id = (w0 + q) * 32 + b;
+            const int64_t id = w * 32 + b;
             if (MODE == MODE_NEW) {
                 U[p] = id;
                 pos[id] = (int32_t)p;
@@ -247,6 +270,8 @@ bitmap_compact_kernel(uint32_t* __restrict__ front, uint32_t* __restrict__ cand,
             ++p;
             bits &= bits - 1;
         }
+        run += ragg;
+        __syncthreads();  // BlockScan storage reuse
     }
 }
 
@@ -451,11 +476,11 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
         int32_t* cnt_k = out->cnt ? out->cnt + cnt_off : nullptr;
         const int gh = grid_for(bounds[k], 256);
         if (csr->cols_is64)
-            hop_sample_kernel<int64_t><<<gh, 256, 0, s>>>(csr->offsets, (const int64_t*)csr->cols, out->ids, sizes, k, f, k0, k1, nbr_k,
-                                                          cnt_k, cand);
+            hop_sample_kernel<int64_t><<<gh, 256, 0, s>>>(csr->offsets, (const int64_t*)csr->cols, out->ids, sizes, k, f, k0, k1,
+                                                          out->rng_seed_dev, nbr_k, cnt_k, cand);
         else
-            hop_sample_kernel<int32_t><<<gh, 256, 0, s>>>(csr->offsets, (const int32_t*)csr->cols, out->ids, sizes, k, f, k0, k1, nbr_k,
-                                                          cnt_k, cand);
+            hop_sample_kernel<int32_t><<<gh, 256, 0, s>>>(csr->offsets, (const int32_t*)csr->cols, out->ids, sizes, k, f, k0, k1,
+                                                          out->rng_seed_dev, nbr_k, cnt_k, cand);
         dgz::count_launch();
         bitmap_compact_kernel<MODE_NEW><<<(int)l.nchunks, kChunkThreads, 0, s>>>(
             front, cand, status + (size_t)k * l.nchunks, tickets + k, l.nchunks, sizes, k, out->ids, pos, nullptr, nullptr);

@@ -81,7 +81,7 @@ class SampleOut(ctypes.Structure):
                 ("sizes_host", ctypes.c_void_p), ("nbr", ctypes.c_void_p), ("nbr_local", ctypes.c_void_p),
                 ("cnt", ctypes.c_void_p), ("blocks_cap", ctypes.c_int64), ("cnt_cap", ctypes.c_int64),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("ids_sorted", ctypes.c_void_p), ("ids_sorted_pos", ctypes.c_void_p)]
+                ("ids_sorted", ctypes.c_void_p), ("ids_sorted_pos", ctypes.c_void_p), ("rng_seed_dev", ctypes.c_void_p)]
 
 
 _vp, _i64, _i32, _u64, _u32, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
@@ -365,7 +365,7 @@ class SampleBuffers:
     """Caller-owned outputs + workspace of dgz_sample_uniform, sized by dgz_sample_bounds."""
 
     def __init__(self, n_nodes: int, max_seeds: int, fanouts, device=None, blocks: bool = True, local: bool = True,
-                 sorted_ids: bool = True):
+                 sorted_ids: bool = True, device_rng: bool = False):
         device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.fanouts = tuple(int(f) for f in fanouts)
         self.bounds, be, ce = sample_bounds(n_nodes, max_seeds, self.fanouts)
@@ -380,9 +380,11 @@ class SampleBuffers:
         self.ids_sorted_pos = torch.empty_like(self.ids) if sorted_ids else None
         wsb = sample_workspace_bytes(n_nodes, max_seeds)
         self.workspace = torch.empty(wsb, dtype=torch.uint8, device=device)
+        self.rng_dev = torch.zeros(1, dtype=torch.int64, device=device) if device_rng else None
         self.struct = SampleOut(self.ids.data_ptr(), self.ids.numel(), self.sizes_dev.data_ptr(), self.sizes_host.data_ptr(),
                                 _dptr(self.nbr), _dptr(self.local), _dptr(self.cnt), be, ce,
-                                self.workspace.data_ptr(), wsb, _dptr(self.ids_sorted), _dptr(self.ids_sorted_pos))
+                                self.workspace.data_ptr(), wsb, _dptr(self.ids_sorted), _dptr(self.ids_sorted_pos),
+                                _dptr(self.rng_dev))
 
     def hop_blocks(self, sizes=None):
         """Per-hop (nbr [n_k x f_k], cnt [n_k], local [n_k x f_k]) views (after a sync)."""

@@ -58,7 +58,7 @@ class MinibatchFetcher:
 
     def __init__(self, table: dgz.Table, graph: dgz.Graph, fanouts, max_seeds: int, slots: int = 2,
                  gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None,
-                 overlap_sampling: bool = False, sample_stream=None, sampler_sms: int = 8):
+                 overlap_sampling: bool = False, sample_stream=None, sampler_sms: int = 8, graphs: bool = False):
         self.table, self.graph = table, graph
         self.fanouts = tuple(int(f) for f in fanouts)
         self.max_seeds = max_seeds
@@ -66,6 +66,10 @@ class MinibatchFetcher:
         # high priority: the fetch's few CTAs are scheduled ahead of the consumer's as SMs free up
         self.partition = None
         self.mode = "sequential"
+        self.graphs = graphs
+        if graphs:                        # one CUDA graph per slot on ordinary streams
+            sampler_sms = 0
+            overlap_sampling = False
         if fetch_stream is None and sample_stream is None and sampler_sms > 0 and not overlap_sampling:
             try:
                 self.partition = dgz.Partition(sampler_sms, -1, dgz.PARTITION_SPREAD)
@@ -86,7 +90,10 @@ class MinibatchFetcher:
             self.sample_stream = sample_stream
             self.mode = "caller-provided sampler stream"
         self.bufs = [dgz.SampleBuffers(graph.n_nodes, max_seeds, self.fanouts, blocks=blocks, local=blocks,
-                                       sorted_ids=True) for _ in range(slots)]
+                                       sorted_ids=True, device_rng=graphs) for _ in range(slots)]
+        self.cuda_graphs = [None] * slots
+        if graphs:
+            self.mode = "sequential, one CUDA graph per slot (sampler + gather replayed as one launch)"
         cap = self.bufs[0].bounds[-1]
         self.rows = [torch.empty((cap, table.row_bytes), dtype=torch.uint8, device="cuda") for _ in range(slots)]
         self.seed_stage = [torch.empty(max_seeds, dtype=torch.int64, device="cuda") for _ in range(slots)]
@@ -122,12 +129,16 @@ class MinibatchFetcher:
         assert n_seeds <= self.max_seeds
         b = self.bufs[p]
         L = len(self.fanouts)
+        if self.graphs and n_seeds == self.max_seeds:
+            return self._fetch_graph(p, seeds, rng_seed, ev, count_into)
         with torch.cuda.stream(ss):
             if ev:
                 ev[0].record(ss)
             if not seeds.is_cuda:
                 self.seed_stage[p][:n_seeds].copy_(seeds, non_blocking=True)   # H2D of the index list
                 seeds = self.seed_stage[p][:n_seeds]
+            if b.rng_dev is not None:
+                b.rng_dev.fill_(_as_i64(rng_seed))
             dgz.sample_uniform(self.graph, seeds, self.fanouts, rng_seed, b, stream=ss)
             self.sampled[p].record(ss)
         gs.wait_event(self.sampled[p])
@@ -142,3 +153,48 @@ class MinibatchFetcher:
                 count_into.copy_(b.sizes_dev[L:L + 1], non_blocking=True)
             self.events[p].record(gs)
         return Minibatch(p, b, self.rows[p], self.events[p], self.fanouts, ev)
+
+    # ---- CUDA-graph mode ----------------------------------------------------------------------
+    def _enqueue_graph_body(self, p):
+        b = self.bufs[p]
+        L = len(self.fanouts)
+        dgz.sample_uniform(self.graph, self.seed_stage[p], self.fanouts, 0, b, stream=self.stream)
+        dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
+                        n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=self.stream)
+
+    def _fetch_graph(self, p, seeds, rng_seed, ev, count_into):
+        """Sampler + gather of slot p as one CUDA-graph replay: seeds and the sampler seed are
+        written into the graph's fixed input buffers first (launch-bound small minibatches)."""
+        s = self.stream
+        b = self.bufs[p]
+        L = len(self.fanouts)
+        if self.cuda_graphs[p] is None:
+            with torch.cuda.stream(s):                  # eager warm-up (allocates lazy state)
+                self.seed_stage[p].copy_(seeds, non_blocking=True)
+                self._enqueue_graph_body(p)
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self._enqueue_graph_body(p)
+            self.cuda_graphs[p] = g
+        with torch.cuda.stream(s):
+            if ev:
+                ev[0].record(s)
+            self.seed_stage[p].copy_(seeds, non_blocking=True)
+            b.rng_dev.fill_(_as_i64(rng_seed))
+            if ev:
+                ev[1].record(s)
+            self.cuda_graphs[p].replay()
+            if ev:
+                ev[2].record(s)
+            if count_into is not None:
+                count_into.copy_(b.sizes_dev[L:L + 1], non_blocking=True)
+            self.sampled[p].record(s)
+            self.events[p].record(s)
+        return Minibatch(p, b, self.rows[p], self.events[p], self.fanouts, ev)
+
+
+def _as_i64(x: int) -> int:
+    """uint64 sampler seed -> the int64 with the same bits (torch tensors are signed)."""
+    x &= (1 << 64) - 1
+    return x - (1 << 64) if x >= (1 << 63) else x

@@ -503,3 +503,29 @@ def test_gather_flag_order(dev, variant):
         assert (got[7] == 0xAB).all() and np.array_equal(got[8:], want[8:])
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("graphs,sampler_sms", [(True, 0), (False, 0), (False, 8)])
+def test_fetcher_modes_match_oracle(dev, graphs, sampler_sms):
+    """MinibatchFetcher in CUDA-graph mode (device-resident sampler seed), sequential mode and the
+    green-context sampler partition all give the oracle's minibatches, step after step."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+    c = gen.CONFIGS[1]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+        f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, graphs=graphs, sampler_sms=sampler_sms)
+        for j in (0, 1, 2, 3, 9):          # j = 9 is the short last batch of the epoch (eager path)
+            seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
+            rs = gen.batch_rng_seed(c.seed, j)
+            mb = f.fetch(torch.from_numpy(seeds).cuda(), rs)
+            n = mb.sizes()[-1]
+            want = oracle.sample_uniform(off, col, seeds, c.fanouts, rs, with_blocks=False)
+            exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+            assert np.array_equal(mb.bufs.ids[:n].cpu().numpy(), want.U), j
+            assert np.array_equal(mb.rows[:n].cpu().numpy(), exp), j
+            f.release(mb)
+        f.close()
+    finally:
+        t.close()
