@@ -472,7 +472,10 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
         except Exception as e:  # green contexts unavailable: report and skip
             rows.append({"fetch_sms": k, "error": str(e)[:200]})
             continue
-        f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream)
+        # grid sized to the partition: one 8-warp CTA per SM, 16 line loads per lane (explore15)
+        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
+        f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream,
+                             gather_cfg=pcfg)
         t_g, t_c, t_o, _ = measure(f, part.compute_stream, repeat=repeat)
         rows.append({"partition": "green context", "fetch_sms": part.fetch_sms, "compute_sms": part.compute_sms,
                      "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
