@@ -276,7 +276,7 @@ bitmap_compact_kernel(uint32_t* __restrict__ front, uint32_t* __restrict__ cand,
 }
 
 // F_0 for up to kSmallSeeds seeds in one block: first occurrence kept, positions recorded
-constexpr int kSmallSeeds = 8192;
+constexpr int kSmallSeeds = 4096;  // 32 KiB of dynamic shared memory: no opt-in attribute needed
 __global__ void __launch_bounds__(1024)
 seeds_small_kernel(const int64_t* __restrict__ seeds, int n, int64_t N, int64_t* __restrict__ U, uint32_t* __restrict__ front,
                    int32_t* __restrict__ pos, int64_t* __restrict__ sizes, int* __restrict__ err) {

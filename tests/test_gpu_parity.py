@@ -241,6 +241,10 @@ def test_sampler_isolated_and_large_seed_set(dev):
     _compare_plan(off, col, gen.batch_seeds(50_000, 9000, 1, 0), (5, 5), 3)
     off, col = gen.gen_csr(200_000, 4.0, 8)
     _compare_plan(off, col, gen.batch_seeds(200_000, 20_000, 8, 1), (3, 2), 4)   # > one seed chunk
+    for ns in (4095, 4096, 4097, 6000):                                          # one-block / multi-kernel seed paths
+        seeds = gen.batch_seeds(200_000, ns, 8, 2)
+        seeds[5] = seeds[3]                                                       # a duplicate
+        _compare_plan(off, col, seeds, (2,), 6)
 
 
 def test_sample_then_gather_device_count(dev):
