@@ -170,7 +170,8 @@ typedef struct {
     int32_t schedule;      /* dgz_gather_schedule */
     int32_t flags;         /* DGZ_GATHER_FLAG_* (SEGMENT variant) */
 } dgz_gather_cfg;
-#define DGZ_GATHER_FLAG_L2_EVICT_FIRST 1 /* zero-copy loads with an L2 evict-first cache policy */
+#define DGZ_GATHER_FLAG_NO_MERGE 1       /* dgz_gather_perm: do not merge the 128 B line two
+                                            table-adjacent rows share (default: merged, R >= 128) */
 #define DGZ_GATHER_FLAG_DEEP 2           /* 16 instead of 8 line loads in flight per lane */
 #define DGZ_GATHER_FLAG_ORDER 4          /* dgz_gather_ex: fetch in table-address order (sort on the
                                             device, gather, scatter back); same result */

@@ -31,20 +31,6 @@ __device__ __forceinline__ uint4 ld_zc_v4(uint64_t p) {
                  : "l"(p));
     return r;
 }
-// same with an L2 evict-first cache policy (keeps the GPU page-table lines resident in L2)
-__device__ __forceinline__ uint4 ld_zc_v4_ef(uint64_t p, uint64_t pol) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
 __device__ __forceinline__ void st_g(uint64_t d, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
@@ -93,7 +79,7 @@ struct CacheArgs {
     const uint8_t* shard[DGZ_MAX_CACHE_SHARDS];
 };
 
-template <int SW, int U, bool HINT, bool CACHED, typename IdxT>
+template <int SW, int U, bool MERGE, bool CACHED, typename IdxT>
 __global__ void __launch_bounds__(512, 1)
 gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
                       const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
@@ -108,7 +94,6 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
     const int sub = lane & 7;
     const uint64_t base = reinterpret_cast<uint64_t>(src);
     const uint64_t dbase = reinterpret_cast<uint64_t>(dst);
-    const uint64_t pol = HINT ? policy_evict_first() : 0;
 
     // Schedule of 32-row batches.  Interleaved: warp w of the grid takes batches w, w + W, ...
     // Blocked (translation-aware): CTA c owns a contiguous range of batches and its warps
@@ -169,7 +154,19 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                 a = reinterpret_cast<uint64_t>(ca.shard[slot % ca.G]) + (uint64_t)(slot / ca.G) * (uint64_t)R;
         }
         const uint64_t l0 = a & ~uint64_t(127);
-        const int nl = id < 0 ? 0 : (int)((a + (uint64_t)R - l0 + 127) >> 7);
+        int nl = id < 0 ? 0 : (int)((a + (uint64_t)R - l0 + 127) >> 7);
+        // MERGE (sorted lists, R >= 128): a row that starts where the previous row of the batch
+        // ends shares that row's last 128 B line; the line is fetched once (by the previous row's
+        // task) and stored to both rows -- one PCIe read per distinct line of the batch, which is
+        // never more than Listing 2's flat enumeration either (SURVEY 8(a) a4')
+        unsigned mmask = 0;
+        if constexpr (MERGE) {
+            const uint64_t a_prev = __shfl_up_sync(0xffffffffu, a, 1);
+            const int64_t id_prev = __shfl_up_sync(0xffffffffu, id, 1);
+            const bool mp = lane > 0 && id >= 0 && id_prev >= 0 && a_prev + (uint64_t)R == a && (a & 127u) != 0;
+            mmask = __ballot_sync(0xffffffffu, mp);
+            nl -= mp ? 1 : 0;
+        }
         int incl = nl;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -196,20 +193,36 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                 const uint64_t ar = __shfl_sync(0xffffffffu, a, sl);
                 const int er = __shfl_sync(0xffffffffu, excl, sl);
                 // chunk = 16 B piece `sub` of line (t - er) of the row's 128 B-aligned segment list
+                // (shifted by one line when the row's first line was merged into the previous row)
+                const int line = t - er + (MERGE ? (int)((mmask >> sl) & 1u) : 0);
                 const int q = (int)(ar & 127u);               // row start offset within its first line
-                const int cq = (t - er) * 128 + sub * 16 - q;  // chunk start relative to the row start
-                const bool act = (t < T) && (cq + 16 > 0) && (cq < (int)R);
+                const int cq = line * 128 + sub * 16 - q;      // chunk start relative to the row start
+                const bool nxt = MERGE && sl < 31 && ((mmask >> (sl + 1)) & 1u);
+                const bool act = (t < T) && (cq + 16 > 0) && (cq < (int)R || nxt);
                 pk[u] = act ? (((cq + 128) << 5) | sl) : -1;
-                if (act) v[u] = HINT ? ld_zc_v4_ef(ar + (uint64_t)(int64_t)cq, pol) : ld_zc_v4(ar + (uint64_t)(int64_t)cq);
+                if (act) v[u] = ld_zc_v4(ar + (uint64_t)(int64_t)cq);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int sl = pk[u] & 31;
                 const int64_t dr = __shfl_sync(0xffffffffu, drow, sl);
+                int64_t dr2 = 0;
+                if constexpr (MERGE) dr2 = __shfl_sync(0xffffffffu, drow, sl < 31 ? sl + 1 : 31);
                 if (pk[u] >= 0) {
                     const int cq = (pk[u] >> 5) - 128;
-                    const uint64_t d = dbase + (uint64_t)dr * (uint64_t)R + (uint64_t)(int64_t)cq;
-                    store_pieces<SW>(d, v[u], cq < 0 ? -cq : 0, (int)R - cq > 16 ? 16 : (int)R - cq);
+                    if (cq < (int)R) {
+                        const uint64_t d = dbase + (uint64_t)dr * (uint64_t)R + (uint64_t)(int64_t)cq;
+                        store_pieces<SW>(d, v[u], cq < 0 ? -cq : 0, (int)R - cq > 16 ? 16 : (int)R - cq);
+                    }
+                    if constexpr (MERGE) {
+                        // bytes past this row's end belong to the next row when it was merged
+                        const bool nxt = sl < 31 && ((mmask >> (sl + 1)) & 1u);
+                        if (nxt && cq + 16 > (int)R) {
+                            const int lo2 = (int)R - cq > 0 ? (int)R - cq : 0;
+                            const uint64_t d2 = dbase + (uint64_t)dr2 * (uint64_t)R + (uint64_t)(int64_t)(cq - (int)R);
+                            store_pieces<SW>(d2, v[u], lo2, 16);
+                        }
+                    }
                 }
             }
         }
@@ -269,13 +282,13 @@ struct SegLaunch {
     cudaStream_t s;
 };
 
-template <int SW, int U, bool HINT, typename IdxT>
+template <int SW, int U, bool MERGE, typename IdxT>
 void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
     if (L.cache) {
-        gather_segment_kernel<SW, U, HINT, true, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
+        gather_segment_kernel<SW, U, MERGE, true, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
             t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache);
     } else {
-        gather_segment_kernel<SW, U, HINT, false, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
+        gather_segment_kernel<SW, U, MERGE, false, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
             t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, CacheArgs{});
     }
     dgz::count_launch();
@@ -283,13 +296,14 @@ void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L)
 
 template <int SW, typename IdxT>
 cudaError_t launch_segment(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
-    const bool hint = L.flags & DGZ_GATHER_FLAG_L2_EVICT_FIRST;
+    // merging shared boundary lines pays only for address-sorted lists of rows >= 128 B
+    const bool merge = L.dst_pos != nullptr && t->row_bytes >= 128 && !(L.flags & DGZ_GATHER_FLAG_NO_MERGE);
     const bool deep = L.flags & DGZ_GATHER_FLAG_DEEP;
     if (deep) {
-        if (hint) launch_segment_k<SW, 16, true>(t, idx, L);
+        if (merge) launch_segment_k<SW, 16, true>(t, idx, L);
         else launch_segment_k<SW, 16, false>(t, idx, L);
     } else {
-        if (hint) launch_segment_k<SW, 8, true>(t, idx, L);
+        if (merge) launch_segment_k<SW, 8, true>(t, idx, L);
         else launch_segment_k<SW, 8, false>(t, idx, L);
     }
     return cudaGetLastError();
@@ -367,7 +381,8 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta
                                                 : (variant == DGZ_GATHER_BULK ? 8 : ((sorted_path && !hbm_table) ? 2 : 16));
     int flags = cfg ? cfg->flags : 0;
-    if (sorted_path && !hbm_table && !bounded && !(cfg && cfg->warps_per_cta > 0) && flags == 0) flags = DGZ_GATHER_FLAG_DEEP;
+    if (sorted_path && !hbm_table && !bounded && !(cfg && cfg->warps_per_cta > 0) && (flags & ~DGZ_GATHER_FLAG_NO_MERGE) == 0)
+        flags |= DGZ_GATHER_FLAG_DEEP;
     const int max_warps = variant == DGZ_GATHER_SEGMENT ? 16 : 32;  // SEGMENT: <= 512 threads (128 regs)
     if (warps > max_warps) warps = max_warps;
     int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : (hbm_table ? 4 : 1);

@@ -332,7 +332,7 @@ def test_bulk_ring_wraparound(dev, R, sms, warps, n):
 
 
 @pytest.mark.parametrize("flags", [0, 1, 2, 3])
-def test_segment_flags(dev, flags):
+def test_segment_flags(dev, flags):   # 1 = NO_MERGE (a no-op without dst_pos), 2 = DEEP
     R, rows = 520, 5000
     t = HostTable(rows, R, seed=flags, base=8, dtype=dgz.F32)
     try:
@@ -531,5 +531,39 @@ def test_fetcher_modes_match_oracle(dev, graphs, sampler_sms):
             assert np.array_equal(mb.rows[:n].cpu().numpy(), exp), j
             f.release(mb)
         f.close()
+    finally:
+        t.close()
+
+
+@pytest.mark.parametrize("R,base", [(400, 0), (520, 8), (512, 4), (512, 0), (2408, 0), (132, 64), (128, 16), (100, 4)])
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_gather_perm_adjacent_rows_merge(dev, R, base, flags):
+    """Sorted lists full of table-adjacent rows: the shared 128 B line of two adjacent rows is
+    fetched once and stored to both (MERGE), chains of adjacent rows, batch boundaries, and the
+    NO_MERGE flag -- byte-identical to the oracle in every case."""
+    rows = 6000
+    t = HostTable(rows, R, seed=R + base, base=base, dtype=dgz.F32)
+    try:
+        runs = [np.arange(s, s + ln) for s, ln in ((0, 40), (100, 3), (777, 64), (2000, 1), (2002, 5), (5990, 10))]
+        idx = np.unique(np.concatenate(runs + [gen.random_ids(rows, 900, seed=R)]))
+        rng = np.random.default_rng(R)
+        shuffled = idx[rng.permutation(idx.shape[0])]
+        want, _ = oracle.gather(t.np, R, shuffled)
+        order = np.argsort(shuffled, kind="stable")
+        ids_s = torch.from_numpy(shuffled[order]).cuda()
+        pos_s = torch.from_numpy(order.astype(np.int64)).cuda()
+        out = torch.full((shuffled.shape[0] * R,), 0xAB, dtype=torch.uint8, device="cuda")
+        for sms in (0, 3):
+            out.fill_(0xAB)
+            dgz.gather_perm(t.table, ids_s, pos_s, out, cfg=dgz.gather_cfg(sm_count=sms, flags=flags))
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy().reshape(-1, R), want), sms
+        # cached rows in consecutive shard slots merge the same way
+        hot = torch.from_numpy(np.arange(770, 900, dtype=np.int64)).cuda()
+        cache = dgz.HotRowCache(t.table, hot)
+        out.fill_(0xAB)
+        cache.gather(ids_s, out, dst_pos=pos_s, cfg=dgz.gather_cfg(flags=flags))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
     finally:
         t.close()
