@@ -86,6 +86,20 @@ def segment_plan_requests(idx_list, row_bytes: int, base: int = 0) -> tuple:
     return total, dict(hist)
 
 
+def merged_plan_requests(sorted_ids, row_bytes: int, base: int = 0, batch: int = 32) -> int:
+    """Requests of the segment plan on an address-sorted list when the 128 B line shared by two
+    table-adjacent rows of the same batch of `batch` rows is fetched once: the number of distinct
+    lines per batch."""
+    total = 0
+    for b0 in range(0, len(sorted_ids), batch):
+        lines = set()
+        for idx in sorted_ids[b0:b0 + batch]:
+            start = base + idx * row_bytes
+            lines.update(range(start // LINE, (start + row_bytes - 1) // LINE + 1))
+        total += len(lines)
+    return total
+
+
 def sector_bytes(idx_list, row_bytes: int, base: int = 0) -> int:
     """Total sector payload bytes (what crosses PCIe, excluding TLP headers)."""
     return sum(SECTOR * row_sectors(base + i * row_bytes, row_bytes) for i in idx_list)

@@ -235,3 +235,20 @@ def test_segment_plan_is_row_minimum():
             assert plan == sum(rm.row_lines(i * feat * 4, feat * 4) for i in ids)
             assert plan <= rm.listing2_requests(ids, feat, shift=True)[0]
             assert plan <= rm.listing2_requests(ids, feat, shift=False)[0]
+
+
+def test_merged_plan_never_exceeds_listing2():
+    """With the shared line of table-adjacent rows fetched once, the segment plan issues no more
+    requests than Listing 2 even on dense sorted lists (where Listing 2's flat enumeration merges
+    such lines too), and exactly the per-row minimum when no two rows are adjacent."""
+    rng = np.random.default_rng(1)
+    for feat in (33, 100, 120, 130, 602):
+        R = feat * 4
+        for _ in range(6):
+            ids = sorted(set(rng.integers(0, 60, size=20).tolist()))      # dense: many adjacent IDs
+            merged = rm.merged_plan_requests(ids, R)
+            assert merged <= rm.segment_plan_requests(ids, R)[0]
+            assert merged <= rm.listing2_requests(ids, feat, shift=True)[0]
+            assert merged <= rm.listing2_requests(ids, feat, shift=False)[0]
+        sparse = [i * 7 for i in range(20)]                                  # no adjacent rows
+        assert rm.merged_plan_requests(sparse, R) == rm.segment_plan_requests(sparse, R)[0]
