@@ -167,6 +167,37 @@ def make_table(cfg, d: Dist, dgz):
     return buf, fill_s
 
 
+def make_csr(cfg, d: Dist, dgz):
+    """The graph's CSR on the host: plain arrays for N = 1; for N > 1 rank 0 generates it once
+    into shared /dev/shm mappings that every rank maps (one host copy per box, not one per rank).
+    Returns (offsets int64 view, cols int32 view, n_edges, keep-alive buffers)."""
+    if d.world == 1:
+        off, col = gen.gen_csr(cfg.n_nodes, cfg.avg_degree, cfg.seed)
+        return off, col, int(off[-1]), []
+    base = f"/dgz_bench_csr{cfg.cid}_{os.environ.get('MASTER_PORT', '0')}"
+    bufs = []
+    e = None
+    if d.rank == 0:
+        def alloc(nb):
+            b = dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{len(bufs)}", create=True)
+            bufs.append(b)
+            return b.ptr
+        gen.set_threads(os.cpu_count() or 1)
+        _, _, e = gen.gen_csr_into(cfg.n_nodes, cfg.avg_degree, cfg.seed, alloc)
+        gen.set_threads(max(1, (os.cpu_count() or 1) // d.world))
+    e = int(d.bcast_obj(e))
+    if d.rank != 0:
+        for i, nb in enumerate(((cfg.n_nodes + 1) * 8, max(e * 4, 1))):
+            bufs.append(dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{i}", create=False))
+    d.barrier()
+    if d.rank == 0:
+        for b in bufs:
+            b.unlink()
+    off = bufs[0].numpy(0, (cfg.n_nodes + 1) * 8).view(np.int64)
+    col = bufs[1].numpy(0, e * 4).view(np.int32)
+    return off, col, e, bufs
+
+
 def ev():
     return torch.cuda.Event(enable_timing=True)
 
@@ -209,6 +240,16 @@ def measure_ceilings(dgz, table_info, R):
             "how": "best of 5 x (cudaMemcpyAsync 256 MiB pinned H2D x10); zero-copy LDG.128 stream over a 1 GiB pinned buffer x4 on 8 SMs"}
 
 
+def hbm_peak() -> float:
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the profiling
+    guide's fallback 6650 GB/s."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def load_profile_traffic(cid):
     """(dram bytes per gather launch, summary) from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_gather_summary.json")
@@ -238,11 +279,12 @@ def run_ours(args, d: Dist):
     table = dgz.register_table(buf.ptr, cfg.n_nodes, cfg.dim, dgz.F32)
     info = table.info
     t0 = time.time()
-    off, col = gen.gen_csr(cfg.n_nodes, cfg.avg_degree, cfg.seed)
+    off, col, n_edges, csr_bufs = make_csr(cfg, d, dgz)
     csr_s = time.time() - t0
-    graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
-    n_edges = int(off[-1])
-    del off, col
+    if args.csr == "host":    # zero-copy CSR (NEXT-3): the sampler reads the host arrays over PCIe
+        graph = dgz.HostGraph(off.ctypes.data, col.ctypes.data, cfg.n_nodes, n_edges, False)
+    else:                     # CSR replicated in each GPU's HBM
+        graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
 
     K, W = args.steps, args.warmup
     G, rank = d.world, d.rank
@@ -313,7 +355,7 @@ def run_ours(args, d: Dist):
     if not args.no_baselines:
         dma_base = run_dma_baseline(cfg, buf, fetcher, graph, seeds_dev, rng, W, K, d)   # every rank, concurrently
         if rank == 0:
-            cpu_base, parity = run_oracle_leg(cfg, buf.ptr, graph, last, d)
+            cpu_base, parity = run_oracle_leg(cfg, buf.ptr, off, col, last, d)
 
     clocks = clk.summary()
     sm_count = torch.cuda.get_device_properties(0).multi_processor_count
@@ -330,6 +372,7 @@ def run_ours(args, d: Dist):
                    "global_batch": cfg.batch * G, "parallelism": f"dp{G} (seed partition j mod G)",
                    "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
                    "pipeline": fetcher.mode,
+                   "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else "pinned host memory, sampled by zero-copy",
                    "gather": {"variant": "segment", "sm_count": args.gather_sms or sm_count_all,
                               "warps_per_cta": args.gather_warps or 2, "lines_in_flight_per_warp": 64,
                               "order": "address-sorted + inverse permutation"}},
@@ -342,7 +385,7 @@ def run_ours(args, d: Dist):
                      "algorithmic_bytes_per_launch": round(float(np.mean(ns)) * R),
                      "gather_ms_mean": round(float(np.mean(gather_ms)), 4),
                      "zc_stream_frac": round(gather_gbs / ceilings["zc_stream_gbs"], 4),
-                     "hbm_write_frac": round(gather_gbs / 6537.3, 5)},
+                     "hbm_write_frac": round(gather_gbs / hbm_peak(), 5)},
         "ceilings": ceilings,
         "latency_ms": {"step_p10": pct(step_ms, 10), "step_p50": pct(step_ms, 50), "step_p90": pct(step_ms, 90),
                        "sample_p50": pct(sample_ms, 50), "gather_p50": pct(gather_ms, 50)},
@@ -357,8 +400,12 @@ def run_ours(args, d: Dist):
                   "csr_gen_s": round(csr_s, 2), "total_s": round(time.time() - t_setup, 1), "sms": sm_count},
     }
     fetcher.close()
+    if args.csr == "host":
+        graph.close()
     table.unregister()
     buf.free()
+    for b in csr_bufs:
+        b.free()
     return line
 
 
@@ -490,12 +537,10 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
             "consumer": "dgz_aggregate_mean over the last hop's block, non-persistent launches, repeated to T_c ~ T_fetch"}
 
 
-def run_oracle_leg(cfg, table_addr, graph, last, d: Dist):
+def run_oracle_leg(cfg, table_addr, off, col, last, d: Dist):
     """cpu_baseline: the oracle as it stands (single-threaded C) on a bounded sample of the
     same workload, plus a full-size exact parity check of the GPU's last two minibatches."""
     import oracle
-    off = graph.offsets.cpu().numpy()
-    col = graph.cols.cpu().numpy()
     R = cfg.row_bytes
     parity = {"batches": [], "exact": True}
     t_total, bytes_total, nb = 0.0, 0, 0
@@ -618,9 +663,12 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
     ap.add_argument("--gather-sms", type=int, default=0)
     ap.add_argument("--gather-warps", type=int, default=0)
-    ap.add_argument("--sampler-sms", type=int, default=8,
-                    help="SMs of the green-context sampler partition (0 = sample and gather back to back)")
+    ap.add_argument("--sampler-sms", type=int, default=None,
+                    help="SMs of the green-context sampler partition (0 = sample and gather back to back; "
+                         "default 8 with the CSR in HBM, 0 with --csr host)")
     ap.add_argument("--graphs", action="store_true", help="replay sampler + gather as one CUDA graph per slot")
+    ap.add_argument("--csr", default="hbm", choices=["hbm", "host"],
+                    help="CSR replicated in HBM (default) or left in pinned host memory and sampled by zero-copy")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false")
     args = ap.parse_args()

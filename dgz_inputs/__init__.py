@@ -89,6 +89,20 @@ def gen_csr(n: int, avg_degree: float, seed: int, col_dtype=np.int32, skew_alpha
     return off, col
 
 
+def gen_csr_into(n: int, avg_degree: float, seed: int, alloc):
+    """gen_csr (int32 columns, uniform endpoints) written into caller memory: ``alloc(nbytes)``
+    returns a writable address (e.g. a shared /dev/shm mapping one rank fills for all).  Returns
+    (offsets address, cols address, n_edges); the bytes equal gen_csr's."""
+    assert n < 2**31
+    po = int(alloc((n + 1) * 8))
+    e = lib().dgz_gen_offsets(n, float(avg_degree), seed, po)
+    if e < 0:
+        raise ValueError("bad graph parameters")
+    pc = int(alloc(max(e * 4, 1)))
+    lib().dgz_gen_cols32(n, e, seed, pc)
+    return po, pc, int(e)
+
+
 def fill_table(buf, nbytes: int, seed: int) -> None:
     """Fill ``nbytes`` bytes at ``buf`` (numpy array or raw address) with keyed random bits."""
     lib().dgz_gen_fill(_ptr(buf), int(nbytes), seed)

@@ -244,8 +244,13 @@ DGZ_API dgz_status dgz_check_errors(dgz_table t, dgz_stream stream);
  * ========================================================================================== */
 typedef struct {
     int64_t n_nodes;
-    const int64_t* offsets; /* device [n_nodes + 1], offsets[0] = 0, non-decreasing */
-    const void* cols;       /* device [offsets[n_nodes]] int32 or int64 node IDs < n_nodes (NULL if no edges) */
+    const int64_t* offsets; /* device-accessible [n_nodes + 1], offsets[0] = 0, non-decreasing */
+    const void* cols;       /* device-accessible [offsets[n_nodes]] int32 or int64 node IDs < n_nodes
+                               (NULL if no edges).  Either HBM, or host memory registered with
+                               dgz_register_table (its dgz_table_info.dev_ptr): the sampler then reads
+                               the CSR by zero-copy loads over PCIe (a CSR that
+                               does not fit HBM); the result is the same either way.  The caller
+                               owns both arrays; they must outlive the call's stream work. */
     int32_t cols_is64;
     int32_t reserved;
 } dgz_csr;

@@ -89,10 +89,21 @@ hop_sample_kernel(const int64_t* __restrict__ off, const ColT* __restrict__ cols
                 pos[b + 1] = v;
             }
         }
-        for (int q = 0; q < c; ++q) {
-            const int64_t s = (int64_t)cols[o0 + pos[q]];
-            if (nbr) nbr[i * f + q] = s;
-            atomicOr(&cand[s >> 5], 1u << (s & 31));
+        // column loads batched 8 at a time ahead of their uses: independent loads in flight per
+        // thread (a zero-copy CSR in host memory pays one PCIe round trip per batch, not per slot)
+        for (int q0 = 0; q0 < c; q0 += 8) {
+            int64_t sv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (q0 + e < c) sv[e] = (int64_t)cols[o0 + pos[q0 + e]];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (q0 + e < c) {
+                    const int64_t s = sv[e];
+                    if (nbr) nbr[i * f + q0 + e] = s;
+                    atomicOr(&cand[s >> 5], 1u << (s & 31));
+                }
+            }
         }
         if (nbr)
             for (int q = c; q < f; ++q) nbr[i * f + q] = -1;

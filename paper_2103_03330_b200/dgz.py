@@ -409,6 +409,50 @@ class Graph:
         self.struct = Csr(self.n_nodes, offsets.data_ptr(), cols.data_ptr(), int(cols.dtype == torch.int64), 0)
 
 
+class HostGraph:
+    """CSR left in pinned, mapped host memory and read by the sampler with zero-copy loads
+    (a graph whose CSR does not fit HBM is sampled where it lies, the way the
+    paper's unified tensor leaves features in host memory).  The offsets and column
+    arrays are registered like feature tables (dgz_register_table as byte tables: pin + map) and
+    the sampler is given their device pointers through the same dgz_csr -- no other change on the
+    path.  ``offsets`` / ``cols`` are host addresses (ints) of int64 [n_nodes + 1] and int32/int64
+    [n_edges] arrays the caller keeps alive, or numpy arrays (copied into HostBuffers here)."""
+
+    def __init__(self, offsets, cols, n_nodes: int | None = None, n_edges: int | None = None,
+                 cols_is64: bool | None = None, flags: int = REG_READONLY):
+        import numpy as np
+        self._owned = []
+        if isinstance(offsets, np.ndarray):
+            assert offsets.dtype == np.int64 and cols.dtype in (np.int32, np.int64)
+            n_nodes, n_edges, cols_is64 = offsets.size - 1, cols.size, cols.dtype == np.int64
+            offsets, cols = self._copy_in(offsets), self._copy_in(cols) if cols.size else 0
+        assert n_nodes is not None and n_edges is not None and cols_is64 is not None
+        self.n_nodes, self.n_edges, self.cols_is64 = int(n_nodes), int(n_edges), bool(cols_is64)
+        self.off_table = register_table(int(offsets), (self.n_nodes + 1) * 8, 1, U8, flags)
+        self.col_table = None
+        col_dev = 0
+        if self.n_edges:
+            self.col_table = register_table(int(cols), self.n_edges * (8 if cols_is64 else 4), 1, U8, flags)
+            col_dev = self.col_table.info.dev_ptr
+        self.struct = Csr(self.n_nodes, self.off_table.info.dev_ptr, col_dev, int(self.cols_is64), 0)
+
+    def _copy_in(self, a) -> int:
+        import numpy as np
+        hb = HostBuffer(max(a.nbytes, 1))
+        np.copyto(hb.numpy(0, a.nbytes).view(a.dtype), a)
+        self._owned.append(hb)
+        return hb.ptr
+
+    def close(self) -> None:
+        for t in (self.col_table, self.off_table):
+            if t is not None:
+                t.unregister()
+        self.col_table = self.off_table = None
+        for hb in self._owned:
+            hb.free()
+        self._owned = []
+
+
 def sample_uniform(graph: Graph, seeds: torch.Tensor, fanouts, rng_seed: int, bufs: SampleBuffers, stream=None) -> SampleBuffers:
     assert seeds.dtype == torch.int64
     fan = _i32arr(list(fanouts))

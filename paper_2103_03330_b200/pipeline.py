@@ -58,8 +58,13 @@ class MinibatchFetcher:
 
     def __init__(self, table: dgz.Table, graph: dgz.Graph, fanouts, max_seeds: int, slots: int = 2,
                  gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None,
-                 overlap_sampling: bool = False, sample_stream=None, sampler_sms: int = 8, graphs: bool = False):
+                 overlap_sampling: bool = False, sample_stream=None, sampler_sms: int | None = None, graphs: bool = False):
         self.table, self.graph = table, graph
+        if sampler_sms is None:
+            # A zero-copy CSR (dgz.HostGraph) makes the sampler a stream of small PCIe reads: beside
+            # the gather both slow down (36 vs 37.8 GB/s sequential, config 4), so it runs back to
+            # back with the gather on the whole GPU; an HBM CSR samples on 8 SMs, hidden.
+            sampler_sms = 0 if isinstance(graph, dgz.HostGraph) else 8
         self.fanouts = tuple(int(f) for f in fanouts)
         self.max_seeds = max_seeds
         self.cfg = gather_cfg
