@@ -1,21 +1,34 @@
-"""GraphSAGE minibatch training fed by the zero-copy fetch pipeline (SURVEY 8(f) NEXT-4 sketch).
+"""GraphSAGE minibatch training fed three ways (the fig:eval_overall analogue).
 
-The paper's application: DGL GraphSAGE training whose node features are gathered by
-zero-copy from host memory.  Here the minibatch (3-hop uniform sample, blocks with positions in U,
-and the gathered fp32 rows in HBM) comes from ``MinibatchFetcher``; the model is plain PyTorch
-(mean aggregator SAGE layers) -- the model is not the hot path, the fetch is.
+The paper's application: DGL GraphSAGE training whose node features live in host
+memory.  Strategies compared on the same minibatches (GPU sampler, same model, same optimizer):
 
-    python examples/graphsage_train.py [--config 4] [--steps 20] [--hidden 256]
+  zc   -- this repo's path: the fetch (sampler + address-sorted zero-copy gather, MinibatchFetcher)
+          runs on a small green-context SM partition while training runs on the rest; step j+1 is
+          fetched while step j trains (MPS X% / (100-X)% in the paper);
+  dma  -- the paper's baseline: the sampled IDs go to the host, CPU threads gather the
+          rows into pinned staging (torch.index_select), cudaMemcpyAsync H2D; double-buffered so the
+          CPU gather of j+1 overlaps the training of j;
+  hbm  -- "All-in-GPU": the whole table copied into HBM once (56.9 GB fits B200's
+          180 GB) and gathered by the same kernel at HBM speed -- the lower bound on step time.
 
-Prints per-minibatch times: fetch alone, train alone, serial (fetch then train) and pipelined
-(fetch of step j+1 on the fetch partition while step j trains), and the loss.
+The model is plain PyTorch (mean-aggregator SAGE layers): it is not the hot path, the
+fetch is.  The table holds random bytes, not meaningful features: inputs are clamped to finite
+values, labels are synthetic (seed ID mod classes).
+
+    python examples/graphsage_train.py [--config 4] [--steps 20] [--modes zc,dma,hbm] [--fetch-sms 16]
+
+Prints one JSON line: per mode the pipelined step time, the training time alone, and speedups.
 """
 import argparse
 import json
 import os
+import queue
 import sys
+import threading
 import time
 
+import numpy as np
 import torch
 import torch.nn.functional as F
 
@@ -51,91 +64,202 @@ class SAGE(torch.nn.Module):
         return h
 
 
+class Trainer:
+    def __init__(self, c, hidden, classes):
+        self.c = c
+        self.classes = classes
+        torch.manual_seed(0)
+        self.model = SAGE(c.dim, hidden, classes, len(c.fanouts)).cuda()
+        self.opt = torch.optim.Adam(self.model.parameters(), lr=1e-3)
+
+    def step(self, rows, bufs, sizes):
+        c = self.c
+        n = sizes[-1]
+        x = torch.nan_to_num(rows[:n].view(torch.float32).view(n, c.dim), nan=0.0, posinf=1.0, neginf=-1.0)
+        x = x.clamp(-1e3, 1e3)
+        labels = (bufs.ids[:sizes[0]] % self.classes).long()        # synthetic labels of the seeds
+        blocks = [(loc, cnt) for (nbr, cnt, loc) in bufs.hop_blocks(sizes)]
+        out = self.model(x, blocks, sizes)
+        loss = F.cross_entropy(out, labels)
+        self.opt.zero_grad(set_to_none=True)
+        loss.backward()
+        self.opt.step()
+        return loss
+
+
+def timed(fn, K):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = fn()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) * 1e3 / K, r
+
+
+def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, trainer, sample_on="compute"):
+    """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
+    sampler (HBM-bound, 0.35 ms on the big partition) runs either in the training stream between
+    steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
+    part = dgz.Partition(fetch_sms, -1, dgz.PARTITION_SPREAD)
+    pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
+    comp = part.compute_stream
+    f = MinibatchFetcher(table, graph, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=pcfg,
+                         sample_stream=comp if sample_on == "compute" else None)
+
+    def fetch_alone():
+        for i in range(K):
+            f.fetch(seeds[i], rng[i]).sizes()
+    for i in range(2):
+        fetch_alone()
+    t_fetch, _ = timed(fetch_alone, K)
+    mb = f.fetch(seeds[0], rng[0])
+    sz = mb.sizes()
+    with torch.cuda.stream(comp):
+        for _ in range(2):
+            trainer.step(mb.rows, mb.bufs, sz)
+        t_train, _ = timed(lambda: [trainer.step(mb.rows, mb.bufs, sz) for _ in range(K)], K)
+    f.release(mb, comp)
+
+    def pipelined():
+        loss = None
+        cur = f.fetch(seeds[0], rng[0])
+        for i in range(1, K + 1):
+            nxt = f.fetch(seeds[i], rng[i])     # fetch j+1 on the fetch partition ...
+            s = cur.sizes()                      # (the host needs |F_k| to slice the blocks)
+            with torch.cuda.stream(comp):
+                comp.wait_event(cur.event)
+                loss = trainer.step(cur.rows, cur.bufs, s)   # ... while j trains on the rest
+            f.release(cur, comp)
+            cur = nxt
+        return loss.detach()
+    pipelined()
+    t_pipe, loss = timed(pipelined, K)
+    out = {"step_ms": round(t_pipe, 3), "fetch_alone_ms": round(t_fetch, 3), "train_alone_ms": round(t_train, 3),
+           "exposed_fetch_ms": round(max(0.0, t_pipe - t_train), 3), "loss": round(float(loss), 4),
+           "fetch_sms": part.fetch_sms, "train_sms": part.compute_sms, "sampler_on": sample_on,
+           "rows_per_minibatch": sz[-1]}
+    f.close()
+    torch.cuda.synchronize()
+    part.destroy()
+    return out
+
+
+def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
+    """The paper's DMA-based method, pipelined: a worker thread samples on the GPU,
+    copies U to the host, gathers the rows with `threads` CPU threads into pinned staging and
+    copies them H2D; the main thread trains on the previous minibatch meanwhile."""
+    torch.set_num_threads(threads)
+    R = c.row_bytes
+    L = len(c.fanouts)
+    bufs = [dgz.SampleBuffers(c.n_nodes, c.batch, c.fanouts, blocks=True, local=True) for _ in range(2)]
+    cap = bufs[0].bounds[-1]
+    stage = [torch.empty((cap, R), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    ids_h = [torch.empty(cap, dtype=torch.int64).pin_memory() for _ in range(2)]
+    rows = [torch.empty((cap, R), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    s_fetch = torch.cuda.Stream()
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    for e in free:
+        e.record()
+    t_cpu = []
+
+    def produce(q, lo, hi):
+        for i in range(lo, hi):
+            p = i % 2
+            free[p].synchronize()                       # slot p's previous training step is done
+            b = bufs[p]
+            with torch.cuda.stream(s_fetch):
+                dgz.sample_uniform(graph, seeds[i], c.fanouts, rng[i], b, stream=s_fetch)
+                s_fetch.synchronize()
+                n = int(b.sizes_host[-1])
+                ids_h[p][:n].copy_(b.ids[:n])            # D2H of the sampled ID list
+                t0 = time.perf_counter()
+                torch.index_select(host_rows, 0, ids_h[p][:n], out=stage[p][:n])   # CPU gather
+                t_cpu.append(time.perf_counter() - t0)
+                rows[p][:n].copy_(stage[p][:n], non_blocking=True)                # H2D DMA
+                ready[p].record(s_fetch)
+            q.put((p, b.sizes_host.tolist()))
+        q.put(None)
+
+    def loop(lo, hi):
+        q = queue.Queue(maxsize=1)
+        th = threading.Thread(target=produce, args=(q, lo, hi), daemon=True)
+        th.start()
+        loss = None
+        while True:
+            item = q.get()
+            if item is None:
+                break
+            p, sz = item
+            cur = torch.cuda.current_stream()
+            cur.wait_event(ready[p])
+            loss = trainer.step(rows[p], bufs[p], sz)
+            free[p].record(cur)
+        th.join()
+        return loss.detach()
+    loop(0, 2)
+    t_cpu.clear()
+
+    def fetch_alone():
+        for i in range(K):
+            p = i % 2
+            b = bufs[p]
+            dgz.sample_uniform(graph, seeds[i], c.fanouts, rng[i], b, stream=s_fetch)
+            s_fetch.synchronize()
+            n = int(b.sizes_host[-1])
+            ids_h[p][:n].copy_(b.ids[:n])
+            torch.index_select(host_rows, 0, ids_h[p][:n], out=stage[p][:n])
+            with torch.cuda.stream(s_fetch):
+                rows[p][:n].copy_(stage[p][:n], non_blocking=True)
+        s_fetch.synchronize()
+    t_fetch, _ = timed(fetch_alone, K)
+    t_pipe, loss = timed(lambda: loop(0, K), K)
+    return {"step_ms": round(t_pipe, 3), "fetch_alone_ms": round(t_fetch, 3), "cpu_gather_ms": round(1e3 * float(np.median(t_cpu)), 3),
+            "cpu_threads": threads, "loss": round(float(loss), 4)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--hidden", type=int, default=256)
     ap.add_argument("--classes", type=int, default=172)      # ogbn-papers100M has 172 classes
+    ap.add_argument("--modes", default="zc,dma,hbm")
+    ap.add_argument("--fetch-sms", type=int, default=16)
+    ap.add_argument("--sample-on", default="compute", choices=["compute", "fetch"])
+    ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))   # one core left for the training loop
     a = ap.parse_args()
     torch.cuda.set_device(0)
+    torch.backends.cuda.matmul.allow_tf32 = True
     c = gen.CONFIGS[a.config]
-    L = len(c.fanouts)
+    K = a.steps
     buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_HUGEPAGE)
     gen.fill_table(buf.ptr, c.table_bytes, c.seed)
-    # the random bytes are not meaningful fp32 features: clamp them to finite values in the model input
     table = dgz.register_table(buf.ptr, c.n_nodes, c.dim, dgz.F32)
     off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
     graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
-    fetcher = MinibatchFetcher(table, graph, c.fanouts, c.batch)
-    model = SAGE(c.dim, a.hidden, a.classes, L).cuda()
-    opt = torch.optim.Adam(model.parameters(), lr=1e-3)
-    K = a.steps
+    del off, col
     seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in range(K + 2)]
     rng = [gen.batch_rng_seed(c.seed, j) for j in range(K + 2)]
-
-    def blocks_of(mb, sizes):
-        b = []
-        for k, (nbr, cnt, loc) in enumerate(mb.bufs.hop_blocks(sizes)):
-            b.append((loc, cnt))
-        return b
-
-    def train_step(mb, sizes):
-        n = sizes[-1]
-        x = torch.nan_to_num(mb.rows[:n].view(torch.float32).view(n, c.dim), nan=0.0, posinf=1.0, neginf=-1.0)
-        x = x.clamp(-1e3, 1e3)
-        labels = (mb.bufs.ids[:sizes[0]] % a.classes).long()     # synthetic labels of the seeds
-        out = model(x, blocks_of(mb, sizes), sizes)
-        loss = F.cross_entropy(out, labels)
-        opt.zero_grad(set_to_none=True)
-        loss.backward()
-        opt.step()
-        return loss
-
-    def timed(fn):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = fn()
-        torch.cuda.synchronize()
-        return (time.perf_counter() - t0) * 1e3 / K, r
-
-    # warm-up
-    for i in range(2):
-        mb = fetcher.fetch(seeds[i], rng[i])
-        train_step(mb, mb.sizes())
-        fetcher.release(mb)          # the slot may be resampled only after this step's kernels
-    t_fetch, _ = timed(lambda: [fetcher.fetch(seeds[i], rng[i]).sizes() for i in range(K)])
-    mb = fetcher.fetch(seeds[0], rng[0])
-    sz = mb.sizes()
-    t_train, _ = timed(lambda: [train_step(mb, sz) for _ in range(K)])
-    fetcher.release(mb)
-
-    def serial():
-        loss = None
-        for i in range(K):
-            m = fetcher.fetch(seeds[i], rng[i])
-            loss = train_step(m, m.sizes())
-            fetcher.release(m)
-        return loss
-    t_serial, _ = timed(serial)
-
-    def pipelined():
-        loss = None
-        cur = fetcher.fetch(seeds[0], rng[0])
-        for i in range(1, K + 1):
-            nxt = fetcher.fetch(seeds[i], rng[i])     # fetch j+1 (fetch partition) ...
-            s = cur.sizes()                            # (host needs |F_k| to slice the blocks)
-            cur.wait()
-            loss = train_step(cur, s)                  # ... while j trains on the default stream
-            fetcher.release(cur)
-            cur = nxt
-        return loss
-    t_pipe, loss = timed(pipelined)
-    print(json.dumps({"config": c.name, "pipeline": fetcher.mode, "rows_per_minibatch": sz[-1],
-                      "fetch_ms": round(t_fetch, 3), "train_ms": round(t_train, 3), "serial_ms": round(t_serial, 3),
-                      "pipelined_ms": round(t_pipe, 3), "exposed_fetch_ms": round(max(0.0, t_pipe - t_train), 3),
-                      "loss": round(float(loss), 4)}))
-    fetcher.close()
+    res = {"config": c.name, "steps": K, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
+                                                   f"{a.classes} classes, Adam, fp32 (TF32 matmuls)"}
+    modes = a.modes.split(",")
+    if "zc" in modes:
+        res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes), a.sample_on)
+    if "dma" in modes:
+        host_rows = torch.from_numpy(buf.numpy(0, c.table_bytes)).view(c.n_nodes, c.row_bytes)
+        res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, a.threads, Trainer(c, a.hidden, a.classes))
+    if "hbm" in modes:
+        dev = torch.empty(c.table_bytes, dtype=torch.uint8, device="cuda")
+        dev.copy_(torch.from_numpy(buf.numpy(0, c.table_bytes)))
+        dtab = dgz.DeviceTable(dev.data_ptr(), c.n_nodes, c.dim, dgz.F32)
+        res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes), a.sample_on)
+        dtab.unregister()
+        del dev
+    if "zc" in res and "dma" in res:
+        res["speedup_zc_over_dma"] = round(res["dma"]["step_ms"] / res["zc"]["step_ms"], 3)
+    if "zc" in res and "hbm" in res:
+        res["zc_vs_all_in_gpu"] = round(res["hbm"]["step_ms"] / res["zc"]["step_ms"], 3)
+    print(json.dumps(res), flush=True)
     table.unregister()
     buf.free()
 
