@@ -175,6 +175,8 @@ typedef struct {
 #define DGZ_GATHER_FLAG_DEEP 2           /* 16 instead of 8 line loads in flight per lane */
 #define DGZ_GATHER_FLAG_ORDER 4          /* dgz_gather_ex: fetch in table-address order (sort on the
                                             device, gather, scatter back); same result */
+#define DGZ_GATHER_FLAG_STREAM_STORES 8  /* SEGMENT: HBM stores as st.global.cs (evict-first in L2) */
+#define DGZ_GATHER_FLAG_EVICT_FIRST_LOADS 16 /* SEGMENT: zero-copy loads under an L2 evict_first policy */
 
 /* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
  * gathers min(*n_dev, n) rows (n is the capacity), so a gather can follow the sampler on the

@@ -31,8 +31,23 @@ __device__ __forceinline__ uint4 ld_zc_v4(uint64_t p) {
                  : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint4 ld_zc_v4_hint(uint64_t p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void st_g(uint64_t d, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_g_cs(uint64_t d, uint4 v) {  // streaming store: evict-first in L2
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void st_g(uint64_t d, uint2 v) {
     asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(d), "r"(v.x), "r"(v.y) : "memory");
@@ -46,10 +61,11 @@ __device__ __forceinline__ void st_g8(uint64_t d, uint32_t v) {
 }
 
 template <int SW>
-__device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo, int hi) {
+__device__ __forceinline__ void store_pieces(uint64_t d, const uint4& v, int lo, int hi, bool cs = false) {
     // store bytes [lo, hi) of the 16-byte chunk v (lo, hi multiples of SW) at global address d + byte
     if constexpr (SW == 16) {
-        st_g(d, v);
+        if (cs) st_g_cs(d, v);
+        else st_g(d, v);
     } else if constexpr (SW == 8) {
         if (lo <= 0 && hi >= 8) st_g(d, make_uint2(v.x, v.y));
         if (lo <= 8 && hi >= 16) st_g(d + 8, make_uint2(v.z, v.w));
@@ -83,7 +99,7 @@ template <int SW, int U, bool MERGE, bool CACHED, typename IdxT>
 __global__ void __launch_bounds__(512, 1)
 gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
                       const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
-                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked, const CacheArgs ca) {
+                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked, const CacheArgs ca, int hints) {
     int64_t n = n_cap;
     if (n_dev) {
         const int64_t m = *n_dev;
@@ -94,6 +110,11 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
     const int sub = lane & 7;
     const uint64_t base = reinterpret_cast<uint64_t>(src);
     const uint64_t dbase = reinterpret_cast<uint64_t>(dst);
+    // cache hints (DGZ_GATHER_FLAG_STREAM_STORES / _EVICT_FIRST_LOADS): keep the streamed rows from
+    // displacing the GPU page-table lines the MMU walks for the zero-copy loads
+    const bool cs_stores = hints & 1;
+    const bool ef_loads = hints & 2;
+    const uint64_t pol = ef_loads ? l2_evict_first_policy() : 0;
 
     // Schedule of 32-row batches.  Interleaved: warp w of the grid takes batches w, w + W, ...
     // Blocked (translation-aware): CTA c owns a contiguous range of batches and its warps
@@ -200,7 +221,7 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                 const bool nxt = MERGE && sl < 31 && ((mmask >> (sl + 1)) & 1u);
                 const bool act = (t < T) && (cq + 16 > 0) && (cq < (int)R || nxt);
                 pk[u] = act ? (((cq + 128) << 5) | sl) : -1;
-                if (act) v[u] = ld_zc_v4(ar + (uint64_t)(int64_t)cq);
+                if (act) v[u] = ef_loads ? ld_zc_v4_hint(ar + (uint64_t)(int64_t)cq, pol) : ld_zc_v4(ar + (uint64_t)(int64_t)cq);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -212,7 +233,7 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                     const int cq = (pk[u] >> 5) - 128;
                     if (cq < (int)R) {
                         const uint64_t d = dbase + (uint64_t)dr * (uint64_t)R + (uint64_t)(int64_t)cq;
-                        store_pieces<SW>(d, v[u], cq < 0 ? -cq : 0, (int)R - cq > 16 ? 16 : (int)R - cq);
+                        store_pieces<SW>(d, v[u], cq < 0 ? -cq : 0, (int)R - cq > 16 ? 16 : (int)R - cq, cs_stores);
                     }
                     if constexpr (MERGE) {
                         // bytes past this row's end belong to the next row when it was merged
@@ -220,7 +241,7 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
                         if (nxt && cq + 16 > (int)R) {
                             const int lo2 = (int)R - cq > 0 ? (int)R - cq : 0;
                             const uint64_t d2 = dbase + (uint64_t)dr2 * (uint64_t)R + (uint64_t)(int64_t)(cq - (int)R);
-                            store_pieces<SW>(d2, v[u], lo2, 16);
+                            store_pieces<SW>(d2, v[u], lo2, 16, cs_stores);
                         }
                     }
                 }
@@ -282,14 +303,18 @@ struct SegLaunch {
     cudaStream_t s;
 };
 
+inline int hints_of(int flags) {
+    return ((flags & DGZ_GATHER_FLAG_STREAM_STORES) ? 1 : 0) | ((flags & DGZ_GATHER_FLAG_EVICT_FIRST_LOADS) ? 2 : 0);
+}
+
 template <int SW, int U, bool MERGE, typename IdxT>
 void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
     if (L.cache) {
         gather_segment_kernel<SW, U, MERGE, true, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
-            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache);
+            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache, hints_of(L.flags));
     } else {
         gather_segment_kernel<SW, U, MERGE, false, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
-            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, CacheArgs{});
+            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, CacheArgs{}, hints_of(L.flags));
     }
     dgz::count_launch();
 }
@@ -373,16 +398,39 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     const bool bounded = cfg && cfg->sm_count > 0;
     // Defaults measured on B200.  Unsorted lists: the whole GPU keeps as
     // many rows in flight as possible to ride out GPU address-translation misses.  Sorted lists
-    // (dgz_gather_perm): a narrow in-flight window (~200 warps x 8 rows) keeps translations
-    // local and still covers the PCIe bandwidth-delay product; it also leaves SMs free.
+    // (dgz_gather_perm): a narrow in-flight window (1-2 warps per SM, 16 line loads per lane,
+    // shaped by row width and sparsity below) keeps translations local and still covers the PCIe
+    // bandwidth-delay product; it also leaves SMs free.
     const bool sorted_path = dst_pos != nullptr;
     int k = bounded ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : nsm;
     const bool hbm_table = t->flags & DGZ_REG_DEVICE;   // HBM-resident: latency-bound, wants many warps
     int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta
                                                 : (variant == DGZ_GATHER_BULK ? 8 : ((sorted_path && !hbm_table) ? 2 : 16));
     int flags = cfg ? cfg->flags : 0;
-    if (sorted_path && !hbm_table && !bounded && !(cfg && cfg->warps_per_cta > 0) && (flags & ~DGZ_GATHER_FLAG_NO_MERGE) == 0)
+    if (sorted_path && !hbm_table && !bounded && !(cfg && cfg->warps_per_cta > 0) &&
+        (flags & ~(DGZ_GATHER_FLAG_NO_MERGE | DGZ_GATHER_FLAG_STREAM_STORES | DGZ_GATHER_FLAG_EVICT_FIRST_LOADS)) == 0) {
         flags |= DGZ_GATHER_FLAG_DEEP;
+        if (variant == DGZ_GATHER_SEGMENT && !cache) {
+            // Translation-bound regime (explore19-22): below ~1 KiB per row
+            // the rate is set by GPU page walks, and it peaks with FEWER rows (distinct pages) in
+            // flight than the 2-warps-per-SM shape that dense 512 B minibatches want.  Measured rule
+            // (each warp keeps 64 line tasks in flight): rows >= 1 KiB or dense rows of >= 4 lines
+            // (< 80 KiB apart): 2 warps per SM; sparse (> 150 KiB apart): one warp on half the SMs;
+            // otherwise one warp per SM.
+            const int64_t lines = (t->row_bytes + 127) / 128;
+            const double gap = (double)t->rows * (double)t->row_bytes / (double)n;
+            if (lines >= 8 || (lines >= 4 && gap < 80.0 * 1024.0)) {
+                k = nsm;
+                warps = 2;
+            } else if (gap > 150.0 * 1024.0) {
+                k = nsm / 2 > 0 ? nsm / 2 : 1;
+                warps = 1;
+            } else {
+                k = nsm;
+                warps = 1;
+            }
+        }
+    }
     const int max_warps = variant == DGZ_GATHER_SEGMENT ? 16 : 32;  // SEGMENT: <= 512 threads (128 regs)
     if (warps > max_warps) warps = max_warps;
     int cps = (cfg && cfg->ctas_per_sm > 0) ? cfg->ctas_per_sm : (hbm_table ? 4 : 1);

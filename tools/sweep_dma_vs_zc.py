@@ -70,16 +70,17 @@ for R in gen.SWEEP_ROW_BYTES:
         b.record()
         torch.cuda.synchronize()
         t_zc = a.elapsed_time(b) / 3 * 1e-3
-        # dma baseline on the same IDs
-        host_rows = host_all[base:base + rows * R].view(rows, R)
-        ids_cpu = torch.from_numpy(ids_np)
-        dma_gather(host_rows, ids_cpu, R)
-        t0 = time.perf_counter()
-        for _ in range(2):
+        rec = {"R": R, "base": base, "n": n, "zc_gbs": round(n * R / t_zc / 1e9, 2), "zc_mrows_s": round(n / t_zc / 1e6, 1)}
+        if "--zc-only" not in sys.argv:
+            # dma baseline on the same IDs
+            host_rows = host_all[base:base + rows * R].view(rows, R)
+            ids_cpu = torch.from_numpy(ids_np)
             dma_gather(host_rows, ids_cpu, R)
-        t_dma = (time.perf_counter() - t0) / 2
-        print(json.dumps({"R": R, "base": base, "n": n, "zc_gbs": round(n * R / t_zc / 1e9, 2),
-                          "dma_gbs": round(n * R / t_dma / 1e9, 2), "zc_over_dma": round(t_dma / t_zc, 2),
-                          "zc_mrows_s": round(n / t_zc / 1e6, 1), "dma_threads": threads}), flush=True)
+            t0 = time.perf_counter()
+            for _ in range(2):
+                dma_gather(host_rows, ids_cpu, R)
+            t_dma = (time.perf_counter() - t0) / 2
+            rec.update({"dma_gbs": round(n * R / t_dma / 1e9, 2), "zc_over_dma": round(t_dma / t_zc, 2), "dma_threads": threads})
+        print(json.dumps(rec), flush=True)
         tb.unregister()
 buf.free()
