@@ -100,6 +100,19 @@ def merged_plan_requests(sorted_ids, row_bytes: int, base: int = 0, batch: int =
     return total
 
 
+def merged_plan_sectors(sorted_ids, row_bytes: int, base: int = 0, batch: int = 32) -> int:
+    """32 B sectors read by the merged segment plan: the distinct sectors of each batch of `batch`
+    address-sorted rows (a shared boundary line is fetched once, with the sectors of both rows)."""
+    total = 0
+    for b0 in range(0, len(sorted_ids), batch):
+        secs = set()
+        for idx in sorted_ids[b0:b0 + batch]:
+            start = base + idx * row_bytes
+            secs.update(range(start // SECTOR, (start + row_bytes - 1) // SECTOR + 1))
+        total += len(secs)
+    return total
+
+
 def sector_bytes(idx_list, row_bytes: int, base: int = 0) -> int:
     """Total sector payload bytes (what crosses PCIe, excluding TLP headers)."""
     return sum(SECTOR * row_sectors(base + i * row_bytes, row_bytes) for i in idx_list)

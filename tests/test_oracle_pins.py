@@ -252,3 +252,18 @@ def test_merged_plan_never_exceeds_listing2():
             assert merged <= rm.listing2_requests(ids, feat, shift=False)[0]
         sparse = [i * 7 for i in range(20)]                                  # no adjacent rows
         assert rm.merged_plan_requests(sparse, R) == rm.segment_plan_requests(sparse, R)[0]
+
+
+def test_merged_plan_sectors_brute_force():
+    """merged_plan_sectors = distinct 32 B sectors per batch, checked by enumerating every byte
+    address of every row; equals the per-row sector sum when no two rows of a batch share a sector."""
+    rng = np.random.default_rng(2)
+    for R in (100, 128, 400, 516, 2408):
+        for base in (0, 4, 64):
+            ids = sorted(set(rng.integers(0, 90, size=40).tolist()))
+            want = 0
+            for b0 in range(0, len(ids), 32):
+                want += len({(base + i * R + k) // 32 for i in ids[b0:b0 + 32] for k in range(R)})
+            assert rm.merged_plan_sectors(ids, R, base) == want
+            sparse = [i * 9 for i in range(50)]
+            assert rm.merged_plan_sectors(sparse, R, base) == sum(rm.row_sectors(base + i * R, R) for i in sparse)
