@@ -214,6 +214,23 @@ typedef struct {
  * allocate temporary device memory. */
 DGZ_API dgz_status dgz_cache_fill(dgz_table t, const int64_t* hot_ids_dev, int64_t n_hot, const dgz_cache_view* cache,
                                   dgz_stream stream);
+/* dgz_cache_fill for a cache sharded across ranks (one process per GPU):
+ * builds the full slot map on the current device but fetches only shard `local_shard` (this rank's
+ * HBM); the other shards of `cache` may be NULL here and are filled by their owners (map them with
+ * dgz_ipc_open before gathering, and order the fills before the first gather, e.g. by a barrier).
+ * local_shard = -1: every shard, as dgz_cache_fill. */
+DGZ_API dgz_status dgz_cache_fill_local(dgz_table t, const int64_t* hot_ids_dev, int64_t n_hot, const dgz_cache_view* cache,
+                                        int32_t local_shard, dgz_stream stream);
+/* Device memory for shards and CUDA IPC handles to map another rank's shard into this process:
+ * on a different GPU of the box the mapping is a peer mapping and the cached gather reads it by
+ * NVLink loads (peer access enabled lazily); on the same GPU it is plain HBM.  dgz_ipc_open's
+ * pointer stays valid until dgz_ipc_close; the owner must not free the shard before that. */
+typedef struct { unsigned char bytes[64]; } dgz_ipc_handle;
+DGZ_API dgz_status dgz_device_alloc(size_t bytes, void** out);
+DGZ_API dgz_status dgz_device_free(void* dev_ptr);
+DGZ_API dgz_status dgz_ipc_get_handle(void* dev_ptr, dgz_ipc_handle* out);
+DGZ_API dgz_status dgz_ipc_open(const dgz_ipc_handle* handle, void** out);
+DGZ_API dgz_status dgz_ipc_close(void* dev_ptr);
 /* As dgz_gather_perm (dst_pos_dev may be NULL: identity), reading cached rows from HBM and the
  * others by zero-copy from the table: out[dst_pos[k]] = table[idx[k]] either way (byte-exact). */
 DGZ_API dgz_status dgz_gather_cached(dgz_table t, const dgz_cache_view* cache, const int64_t* idx_dev,

@@ -71,6 +71,10 @@ class CacheView(ctypes.Structure):
                 ("shards", ctypes.c_void_p * MAX_CACHE_SHARDS)]
 
 
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_ubyte * 64)]
+
+
 class Csr(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int64), ("offsets", ctypes.c_void_p), ("cols", ctypes.c_void_p),
                 ("cols_is64", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -103,6 +107,12 @@ _SIGS = {
     "dgz_wrap_device_table": ([_vp, _i64, _i64, ctypes.c_int, _P(_vp)], ctypes.c_int),
     "dgz_cache_fill": ([_vp, _vp, _i64, _P(CacheView), _vp], ctypes.c_int),
     "dgz_gather_cached": ([_vp, _P(CacheView), _vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
+    "dgz_cache_fill_local": ([_vp, _vp, _i64, _P(CacheView), _i32, _vp], ctypes.c_int),
+    "dgz_device_alloc": ([_sz, _P(_vp)], ctypes.c_int),
+    "dgz_device_free": ([_vp], ctypes.c_int),
+    "dgz_ipc_get_handle": ([_vp, _P(IpcHandle)], ctypes.c_int),
+    "dgz_ipc_open": ([_P(IpcHandle), _P(_vp)], ctypes.c_int),
+    "dgz_ipc_close": ([_vp], ctypes.c_int),
     "dgz_table_get_info": ([_vp, _P(TableInfo)], ctypes.c_int),
     "dgz_gather": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_gather_i32": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
@@ -282,6 +292,71 @@ class HotRowCache:
                                       _dptr(n_dev), _dptr(out), ctypes.byref(cfg) if cfg is not None else None,
                                       _stream(stream)), "dgz_gather_cached")
         return out
+
+
+class ShardedHotRowCache:
+    """HBM row cache sharded across the ranks of a process group (one process per GPU; SURVEY 8(e),
+    8(f) NEXT-1): rank g owns shard g (hot rows g, g + G, ...) in its own HBM and fills it by
+    zero-copy (dgz_cache_fill_local); the shards' CUDA IPC handles are exchanged once with an
+    object all-gather (setup, off the data path) and every rank maps the others' shards
+    (dgz_ipc_open: NVLink peer memory on an 8-GPU box, the same HBM when ranks share a GPU).  The
+    cached gather then reads each row from whichever GPU holds it, the rest over PCIe.  `group` is
+    a torch.distributed process group (None = default)."""
+
+    def __init__(self, table: Table, hot_ids: torch.Tensor, group=None, stream=None):
+        import torch.distributed as dist
+        assert hot_ids.dtype == torch.int64 and hot_ids.is_cuda
+        G, g = dist.get_world_size(group), dist.get_rank(group)
+        assert 1 <= G <= MAX_CACHE_SHARDS
+        self.table, self.G, self.rank = table, G, g
+        n_hot = hot_ids.numel()
+        per = max((n_hot + G - 1) // G, 1)
+        p = _vp()
+        _check(_lib.dgz_device_alloc(per * table.row_bytes, ctypes.byref(p)), "dgz_device_alloc")
+        self.local = p.value
+        self.slot_map = torch.empty(table.rows, dtype=torch.int32, device=hot_ids.device)
+        self.view = CacheView(self.slot_map.data_ptr(), G, 0)
+        self.view.shards[g] = self.local
+        _check(_lib.dgz_cache_fill_local(table.handle, _dptr(hot_ids) if n_hot else None, n_hot, ctypes.byref(self.view), g,
+                                         _stream(stream)), "dgz_cache_fill_local")
+        (torch.cuda.current_stream() if stream is None else stream).synchronize()
+        h = IpcHandle()
+        _check(_lib.dgz_ipc_get_handle(self.local, ctypes.byref(h)), "dgz_ipc_get_handle")
+        handles = [None] * G
+        dist.all_gather_object(handles, bytes(h.bytes), group=group)   # also orders every fill before use
+        self.opened = []
+        for r, hb in enumerate(handles):
+            if r == g:
+                continue
+            hr = IpcHandle()
+            ctypes.memmove(hr.bytes, hb, 64)
+            q = _vp()
+            _check(_lib.dgz_ipc_open(ctypes.byref(hr), ctypes.byref(q)), "dgz_ipc_open")
+            self.view.shards[r] = q.value
+            self.opened.append(q.value)
+        self.n_hot = n_hot
+        self.group = group
+
+    def gather(self, idx: torch.Tensor, out: torch.Tensor, dst_pos: torch.Tensor | None = None, n: int | None = None,
+               n_dev: torch.Tensor | None = None, cfg: GatherCfg | None = None, stream=None) -> torch.Tensor:
+        n = idx.numel() if n is None else n
+        assert idx.dtype == torch.int64
+        _check(_lib.dgz_gather_cached(self.table.handle, ctypes.byref(self.view), _dptr(idx), _dptr(dst_pos), n,
+                                      _dptr(n_dev), _dptr(out), ctypes.byref(cfg) if cfg is not None else None,
+                                      _stream(stream)), "dgz_gather_cached")
+        return out
+
+    def close(self) -> None:
+        """Collective: unmap the peers' shards, then (after every rank has) free this rank's shard."""
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        for q in self.opened:
+            _check(_lib.dgz_ipc_close(q), "dgz_ipc_close")
+        self.opened = []
+        dist.barrier(group=self.group)
+        if self.local:
+            _check(_lib.dgz_device_free(self.local), "dgz_device_free")
+            self.local = None
 
 
 def unregister_table(t: Table) -> None:
