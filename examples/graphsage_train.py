@@ -17,6 +17,7 @@ fetch is.  The table holds random bytes, not meaningful features: inputs are cla
 values, labels are synthetic (seed ID mod classes).
 
     python examples/graphsage_train.py [--config 4] [--steps 20] [--modes zc,dma,hbm] [--fetch-sms 16]
+    torchrun --nproc-per-node N examples/graphsage_train.py --modes zc,dma     (DDP, one process per GPU)
 
 Prints one JSON line: per mode the pipelined step time, the training time alone, and speedups.
 """
@@ -65,11 +66,13 @@ class SAGE(torch.nn.Module):
 
 
 class Trainer:
-    def __init__(self, c, hidden, classes):
+    def __init__(self, c, hidden, classes, ddp: bool = False):
         self.c = c
         self.classes = classes
         torch.manual_seed(0)
         self.model = SAGE(c.dim, hidden, classes, len(c.fanouts)).cuda()
+        if ddp:   # data parallel over the ranks: gradients all-reduced by DDP (not the fetch path)
+            self.model = torch.nn.parallel.DistributedDataParallel(self.model, device_ids=[torch.cuda.current_device()])
         self.opt = torch.optim.Adam(self.model.parameters(), lr=1e-3)
 
     def step(self, rows, bufs, sizes):
@@ -228,39 +231,75 @@ def main():
     ap.add_argument("--sample-on", default="compute", choices=["compute", "fetch"])
     ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))   # one core left for the training loop
     a = ap.parse_args()
-    torch.cuda.set_device(0)
+    # one process per GPU under torchrun (DDP; DGZ_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 with gloo)
+    G = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    same = os.environ.get("DGZ_BENCH_SAME_DEVICE") == "1"
+    dev_id = 0 if same else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev_id)
+    dist = None
+    if G > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo" if same else "nccl")
     torch.backends.cuda.matmul.allow_tf32 = True
     c = gen.CONFIGS[a.config]
     K = a.steps
-    buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_HUGEPAGE)
-    gen.fill_table(buf.ptr, c.table_bytes, c.seed)
+    if G == 1:
+        buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_HUGEPAGE)
+        gen.fill_table(buf.ptr, c.table_bytes, c.seed)
+    else:   # one host table per box, registered by every rank
+        name = f"/dgz_train_{os.environ.get('MASTER_PORT', '0')}"
+        if rank == 0:
+            buf = dgz.HostBuffer(c.table_bytes + 4096, shm_name=name, create=True)
+            gen.fill_table(buf.ptr, c.table_bytes, c.seed)
+        dist.barrier()
+        if rank != 0:
+            buf = dgz.HostBuffer(c.table_bytes + 4096, shm_name=name, create=False)
+        dist.barrier()
+        if rank == 0:
+            buf.unlink()
     table = dgz.register_table(buf.ptr, c.n_nodes, c.dim, dgz.F32)
     off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
     graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
     del off, col
-    seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in range(K + 2)]
-    rng = [gen.batch_rng_seed(c.seed, j) for j in range(K + 2)]
-    res = {"config": c.name, "steps": K, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
-                                                   f"{a.classes} classes, Adam, fp32 (TF32 matmuls)"}
+    batches = [i * G + rank for i in range(K + 2)]          # seed partition: global batch j = i*G + rank
+    seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in batches]
+    rng = [gen.batch_rng_seed(c.seed, j) for j in batches]
+    res = {"config": c.name, "steps": K, "ranks": G, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
+                                                              f"{a.classes} classes, Adam, fp32 (TF32 matmuls)"
+                                                              + (", DDP" if G > 1 else "")}
     modes = a.modes.split(",")
+    threads = max(1, a.threads // G)
     if "zc" in modes:
-        res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes), a.sample_on)
+        res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes, G > 1),
+                                     a.sample_on)
     if "dma" in modes:
         host_rows = torch.from_numpy(buf.numpy(0, c.table_bytes)).view(c.n_nodes, c.row_bytes)
-        res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, a.threads, Trainer(c, a.hidden, a.classes))
+        res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, Trainer(c, a.hidden, a.classes, G > 1))
     if "hbm" in modes:
         dev = torch.empty(c.table_bytes, dtype=torch.uint8, device="cuda")
         dev.copy_(torch.from_numpy(buf.numpy(0, c.table_bytes)))
         dtab = dgz.DeviceTable(dev.data_ptr(), c.n_nodes, c.dim, dgz.F32)
-        res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes), a.sample_on)
+        res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes, G > 1),
+                                      a.sample_on)
         dtab.unregister()
         del dev
+    if G > 1:   # per-rank results to rank 0; the job's step time is the slowest rank's
+        allres = [None] * G
+        dist.all_gather_object(allres, {m: res[m] for m in ("zc", "dma", "hbm") if m in res})
+        for m in ("zc", "dma", "hbm"):
+            if m in res:
+                res[m] = {"step_ms": max(r[m]["step_ms"] for r in allres), "per_rank": [r[m] for r in allres]}
     if "zc" in res and "dma" in res:
         res["speedup_zc_over_dma"] = round(res["dma"]["step_ms"] / res["zc"]["step_ms"], 3)
     if "zc" in res and "hbm" in res:
         res["zc_vs_all_in_gpu"] = round(res["hbm"]["step_ms"] / res["zc"]["step_ms"], 3)
-    print(json.dumps(res), flush=True)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
     table.unregister()
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     buf.free()
 
 
