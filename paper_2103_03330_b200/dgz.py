@@ -314,17 +314,23 @@ class ShardedHotRowCache:
         p = _vp()
         _check(_lib.dgz_device_alloc(per * table.row_bytes, ctypes.byref(p)), "dgz_device_alloc")
         self.local = p.value
+        self.opened = []
+        self.group = group
         self.slot_map = torch.empty(table.rows, dtype=torch.int32, device=hot_ids.device)
         self.view = CacheView(self.slot_map.data_ptr(), G, 0)
         self.view.shards[g] = self.local
-        _check(_lib.dgz_cache_fill_local(table.handle, _dptr(hot_ids) if n_hot else None, n_hot, ctypes.byref(self.view), g,
-                                         _stream(stream)), "dgz_cache_fill_local")
-        (torch.cuda.current_stream() if stream is None else stream).synchronize()
         h = IpcHandle()
-        _check(_lib.dgz_ipc_get_handle(self.local, ctypes.byref(h)), "dgz_ipc_get_handle")
+        try:
+            _check(_lib.dgz_cache_fill_local(table.handle, _dptr(hot_ids) if n_hot else None, n_hot, ctypes.byref(self.view),
+                                             g, _stream(stream)), "dgz_cache_fill_local")
+            (torch.cuda.current_stream() if stream is None else stream).synchronize()
+            _check(_lib.dgz_ipc_get_handle(self.local, ctypes.byref(h)), "dgz_ipc_get_handle")
+        except Exception:
+            _lib.dgz_device_free(self.local)
+            self.local = None
+            raise
         handles = [None] * G
         dist.all_gather_object(handles, bytes(h.bytes), group=group)   # also orders every fill before use
-        self.opened = []
         for r, hb in enumerate(handles):
             if r == g:
                 continue
@@ -335,12 +341,12 @@ class ShardedHotRowCache:
             self.view.shards[r] = q.value
             self.opened.append(q.value)
         self.n_hot = n_hot
-        self.group = group
 
     def gather(self, idx: torch.Tensor, out: torch.Tensor, dst_pos: torch.Tensor | None = None, n: int | None = None,
                n_dev: torch.Tensor | None = None, cfg: GatherCfg | None = None, stream=None) -> torch.Tensor:
         n = idx.numel() if n is None else n
         assert idx.dtype == torch.int64
+        assert self.local is not None, "ShardedHotRowCache is closed"
         _check(_lib.dgz_gather_cached(self.table.handle, ctypes.byref(self.view), _dptr(idx), _dptr(dst_pos), n,
                                       _dptr(n_dev), _dptr(out), ctypes.byref(cfg) if cfg is not None else None,
                                       _stream(stream)), "dgz_gather_cached")
@@ -503,12 +509,16 @@ class HostGraph:
             offsets, cols = self._copy_in(offsets), self._copy_in(cols) if cols.size else 0
         assert n_nodes is not None and n_edges is not None and cols_is64 is not None
         self.n_nodes, self.n_edges, self.cols_is64 = int(n_nodes), int(n_edges), bool(cols_is64)
-        self.off_table = register_table(int(offsets), (self.n_nodes + 1) * 8, 1, U8, flags)
-        self.col_table = None
-        col_dev = 0
-        if self.n_edges:
-            self.col_table = register_table(int(cols), self.n_edges * (8 if cols_is64 else 4), 1, U8, flags)
-            col_dev = self.col_table.info.dev_ptr
+        self.off_table = self.col_table = None
+        try:
+            self.off_table = register_table(int(offsets), (self.n_nodes + 1) * 8, 1, U8, flags)
+            col_dev = 0
+            if self.n_edges:
+                self.col_table = register_table(int(cols), self.n_edges * (8 if cols_is64 else 4), 1, U8, flags)
+                col_dev = self.col_table.info.dev_ptr
+        except Exception:
+            self.close()
+            raise
         self.struct = Csr(self.n_nodes, self.off_table.info.dev_ptr, col_dev, int(self.cols_is64), 0)
 
     def _copy_in(self, a) -> int:
