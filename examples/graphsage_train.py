@@ -98,7 +98,7 @@ def timed(fn, K):
     return (time.perf_counter() - t0) * 1e3 / K, r
 
 
-def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, trainer, sample_on="compute"):
+def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute"):
     """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
     sampler (HBM-bound, 0.35 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
@@ -107,6 +107,9 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, trainer, sample_
     comp = part.compute_stream
     f = MinibatchFetcher(table, graph, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=pcfg,
                          sample_stream=comp if sample_on == "compute" else None)
+    with torch.cuda.stream(comp):   # model (and DDP's buckets) created on the stream that trains
+        trainer = make_trainer()
+    torch.cuda.synchronize()
 
     def fetch_alone():
         for i in range(K):
@@ -271,8 +274,8 @@ def main():
     modes = a.modes.split(",")
     threads = max(1, a.threads // G)
     if "zc" in modes:
-        res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes, G > 1),
-                                     a.sample_on)
+        res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms,
+                                     lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on)
     if "dma" in modes:
         host_rows = torch.from_numpy(buf.numpy(0, c.table_bytes)).view(c.n_nodes, c.row_bytes)
         res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, Trainer(c, a.hidden, a.classes, G > 1))
@@ -280,8 +283,8 @@ def main():
         dev = torch.empty(c.table_bytes, dtype=torch.uint8, device="cuda")
         dev.copy_(torch.from_numpy(buf.numpy(0, c.table_bytes)))
         dtab = dgz.DeviceTable(dev.data_ptr(), c.n_nodes, c.dim, dgz.F32)
-        res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms, Trainer(c, a.hidden, a.classes, G > 1),
-                                      a.sample_on)
+        res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms,
+                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on)
         dtab.unregister()
         del dev
     if G > 1:   # per-rank results to rank 0; the job's step time is the slowest rank's

@@ -53,3 +53,37 @@ def test_full_size_config(cid):
     finally:
         table.unregister()
         buf.free()
+
+
+def test_output_beyond_4gib():
+    """64-bit destination offsets: 10.5 M rows of 512 B (5.4 GB of output) gathered from a 2 GB
+    table, unsorted and address-sorted; sampled rows (every 997th plus the last 64) byte-exact."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2103_03330_b200 import dgz
+    torch.cuda.set_device(0)
+    R, rows, n = 512, 4_000_000, 10_500_000
+    buf = dgz.HostBuffer(rows * R + 4096)
+    gen.fill_table(buf.ptr, rows * R, 99)
+    table = dgz.register_table(buf.ptr, rows, R // 4, dgz.F32)
+    try:
+        idx_np = gen.random_ids(rows, n, seed=4)
+        idx = torch.from_numpy(idx_np).cuda()
+        out = torch.empty(n * R, dtype=torch.uint8, device="cuda")
+        pick = np.concatenate([np.arange(0, n, 997), np.arange(n - 64, n)])
+        exp = np.empty(pick.shape[0] * R, dtype=np.uint8)
+        assert oracle.gather_into(buf.ptr, rows, R, idx_np[pick], exp) == 0
+        exp = exp.reshape(-1, R)
+        pk = torch.from_numpy(pick).cuda()
+        dgz.gather(table, idx, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.view(n, R)[pk].cpu().numpy(), exp)
+        srt, pos = dgz.order_ids(idx, rows)
+        out.zero_()
+        dgz.gather_perm(table, srt, pos, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.view(n, R)[pk].cpu().numpy(), exp)
+        dgz.check_errors(table)
+    finally:
+        table.unregister()
+        buf.free()
