@@ -537,13 +537,18 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
             continue
         # grid sized to the partition: one 8-warp CTA per SM, 16 line loads per lane (explore15)
         pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
-        f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream,
-                             gather_cfg=pcfg)
-        t_g, t_c, t_o, _ = measure(f, part.compute_stream, repeat=repeat)
-        rows.append({"partition": "green context", "fetch_sms": part.fetch_sms, "compute_sms": part.compute_sms,
-                     "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
-                     "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
-                     "fetch_gbs_alone": round(float(f.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2)})
+        # sampler placement: in front of the gather on the small partition, or in the consumer's stream
+        # between consumer steps (its full-partition bitmap passes then run beside the gather and slow
+        # its page walks, but it leaves the small partition; DESIGN 5) -- both measured
+        for where in ("fetch partition", "consumer stream"):
+            f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream,
+                                 gather_cfg=pcfg, sample_stream=part.compute_stream if where == "consumer stream" else None)
+            t_g, t_c, t_o, _ = measure(f, part.compute_stream, repeat=repeat)
+            rows.append({"partition": f"green context, sampler in the {where}", "fetch_sms": part.fetch_sms,
+                         "compute_sms": part.compute_sms,
+                         "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
+                         "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
+                         "fetch_gbs_alone": round(float(f.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2)})
         del f
         torch.cuda.synchronize()
         part.destroy()
