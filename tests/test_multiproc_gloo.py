@@ -38,6 +38,8 @@ def _worker(rank, world, port, q):
         K = 3
         mine = [i * world + rank for i in range(K)]
         off, col = gen.gen_csr(cfg.n_nodes, cfg.avg_degree, cfg.seed)
+        off2, col2, e2, csr_bufs = bench.make_csr(cfg, d, dgz)          # one CSR per box in /dev/shm
+        ok_csr = bool(e2 == off[-1] and np.array_equal(off2, off) and np.array_equal(col2, col))
         sizes = []
         for j in mine:
             s = oracle.sample_uniform(off, col, gen.batch_seeds(cfg.n_nodes, cfg.batch, cfg.seed, j), cfg.fanouts,
@@ -47,8 +49,10 @@ def _worker(rank, world, port, q):
         mx, = d.allreduce([float(rank + 1)], "max")
         d.barrier()
         buf.free()
+        for b in csr_bufs:
+            b.free()
         d.close()
-        q.put((rank, ok_table, mine, sizes, tot, mx))
+        q.put((rank, ok_table and ok_csr, mine, sizes, tot, mx))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
 
@@ -67,7 +71,7 @@ def test_two_ranks_share_table_and_partition_batches():
         res[r[0]] = r
     for p in ps:
         p.join(timeout=60)
-    assert res[0][1] and res[1][1]                                   # both ranks see the same table bytes
+    assert res[0][1] and res[1][1]                                   # both ranks see the same table and CSR bytes
     assert sorted(res[0][2] + res[1][2]) == list(range(6))           # j = i*G + rank: disjoint cover
     assert res[0][4] == res[1][4] == sum(res[0][3]) + sum(res[1][3])  # all-reduce SUM of bytes
     assert res[0][5] == res[1][5] == 2.0                              # MAX over ranks
