@@ -339,7 +339,6 @@ def run_ours(args, d: Dist):
     bytes_rank = float(sum(ns) * R)
     tm = [mbs[i].timing for i in range(W, W + K)]
     gather_ms = [t[1].elapsed_time(t[2]) for t in tm]
-    sample_ms = [t[0].elapsed_time(t[1]) for t in tm]   # sample + wait for the previous gather
     step_ms = [t[0].elapsed_time(t[2]) for t in tm]
     tot_bytes, = d.allreduce([bytes_rank], "sum")
     max_el, = d.allreduce([elapsed], "max")
@@ -357,6 +356,9 @@ def run_ours(args, d: Dist):
 
     # ---- end-to-end through the public API: pinned host seeds -> H2D -> sample -> gather -> D2H |U|
     e2e = run_e2e(fetcher, cfg, seeds_host, rng, W, K, d)
+
+    # ---- minibatch-fetch latency, unpipelined: sampling then gather of one minibatch on one stream
+    lat = run_latency(fetcher, cfg, seeds_dev, rng, min(K, 16))
 
     # ---- overlap with a stand-in consumer (steps a5-a7)
     overlap = run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K) if (args.overlap and rank == 0) else None
@@ -403,8 +405,11 @@ def run_ours(args, d: Dist):
                                    "what": f"whole-job step GB/s over {G} rank(s) vs the H2D DMA / zero-copy ceilings "
                                            "measured on all ranks at once (host root-complex limit)"}},
         "ceilings": ceilings,
-        "latency_ms": {"step_p10": pct(step_ms, 10), "step_p50": pct(step_ms, 50), "step_p90": pct(step_ms, 90),
-                       "sample_p50": pct(sample_ms, 50), "gather_p50": pct(gather_ms, 50)},
+        "latency_ms": {"fetch": lat,
+                       "pipelined": {"gather_p10": pct(gather_ms, 10), "gather_p50": pct(gather_ms, 50),
+                                     "gather_p90": pct(gather_ms, 90), "sample_to_gather_end_p50": pct(step_ms, 50),
+                                     "note": "in the pipeline the sampling of j+1 starts during the gather of j, so "
+                                             "sample start -> gather end spans about two gathers"}},
         "rows_per_step_mean": round(float(np.mean(ns)), 1),
         "cpu_baseline": cpu_base, "dma_baseline": dma_base, "parity": parity,
         "e2e": e2e, "overlap": overlap,
@@ -427,6 +432,28 @@ def run_ours(args, d: Dist):
 
 def pct(xs, q):
     return round(float(np.percentile(xs, q)), 4)
+
+
+def run_latency(fetcher, cfg, seeds_dev, rng, n):
+    """Minibatch-fetch latency without pipelining: on one stream, sample (whole GPU) then gather,
+    events around each phase; p10/p50/p90 over n fresh minibatches."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+    f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, sampler_sms=0)
+    for i in range(2):
+        f.fetch(seeds_dev[i], rng[i]).event.synchronize()
+    samp, gath, tot = [], [], []
+    for i in range(n):
+        mb = f.fetch(seeds_dev[i], rng[i], timing=True)
+        mb.event.synchronize()
+        t0, t1, t2 = mb.timing
+        samp.append(t0.elapsed_time(t1))
+        gath.append(t1.elapsed_time(t2))
+        tot.append(t0.elapsed_time(t2))
+    out = {}
+    for k, xs in (("sample", samp), ("gather", gath), ("sample_plus_gather", tot)):
+        out.update({f"{k}_p10": pct(xs, 10), f"{k}_p50": pct(xs, 50), f"{k}_p90": pct(xs, 90)})
+    out["minibatches"] = n
+    return out
 
 
 def run_e2e(fetcher, cfg, seeds_host, rng, W, K, d: Dist):
