@@ -567,3 +567,26 @@ def test_gather_perm_adjacent_rows_merge(dev, R, base, flags):
         assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("R,rows,n", [(128, 4_000_000, 3000),     # > 150 KiB apart: half the SMs, 1 warp
+                                      (128, 400_000, 60_000),      # dense small rows: every SM, 1 warp
+                                      (400, 2_000_000, 5000),      # 4 lines, sparse: 1 warp per SM
+                                      (400, 200_000, 80_000),      # 4 lines, dense: 2 warps per SM
+                                      (1028, 600_000, 2000),       # >= 8 lines: 2 warps per SM
+                                      (64, 8_000_000, 1000)])
+def test_gather_perm_default_launch_shapes(dev, R, rows, n):
+    """Every branch of the sorted gather's default launch-shape rule (row width x sparsity) moves the
+    same bytes as the oracle."""
+    t = HostTable(rows, R, seed=R + n, base=4, dtype=dgz.F32)
+    try:
+        idx = gen.random_ids(rows, n, seed=n)
+        want, _ = oracle.gather(t.np, R, idx)
+        srt, pos = dgz.order_ids(torch.from_numpy(idx).cuda(), rows)
+        out = torch.full((n * R,), 0xAB, dtype=torch.uint8, device="cuda")
+        dgz.gather_perm(t.table, srt, pos, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(n, R), want)
+        dgz.check_errors(t.table)
+    finally:
+        t.close()
