@@ -29,6 +29,9 @@ void set_error(const char* fmt, ...) {
 
 dgz_status cuda_fail(cudaError_t e, const char* what) {
     set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    // the failure is reported here: clear the runtime's last-error state so a non-sticky error
+    // (e.g. an invalid IPC handle) does not resurface in the next call's launch check
+    (void)cudaGetLastError();
     return DGZ_ERR_CUDA;
 }
 
