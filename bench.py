@@ -151,8 +151,9 @@ def make_table(cfg, d: Dist, dgz):
     else:
         name = f"/dgz_bench_c{cfg.cid}_{os.environ.get('MASTER_PORT', '0')}"
         fill_s = 0.0
-        if d.rank == 0:
-            buf = dgz.HostBuffer(nbytes + 4096, shm_name=name, create=True, flags=dgz.HOST_HUGEPAGE)
+        if d.rank == 0:   # interleaved over the sockets' memory when the box has several NUMA nodes
+            buf = dgz.HostBuffer(nbytes + 4096, shm_name=name, create=True,
+                                 flags=dgz.HOST_HUGEPAGE | dgz.HOST_NUMA_INTERLEAVE)
             t0 = time.time()
             gen.set_threads(os.cpu_count() or 1)      # the other ranks are waiting: use every core
             gen.fill_table(buf.ptr, nbytes, cfg.seed)
@@ -179,7 +180,7 @@ def make_csr(cfg, d: Dist, dgz):
     e = None
     if d.rank == 0:
         def alloc(nb):
-            b = dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{len(bufs)}", create=True)
+            b = dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{len(bufs)}", create=True, flags=dgz.HOST_NUMA_INTERLEAVE)
             bufs.append(b)
             return b.ptr
         gen.set_threads(os.cpu_count() or 1)
@@ -418,7 +419,10 @@ def run_ours(args, d: Dist):
         "setup": {"table_fill_s": round(fill_s, 2), "register_s": round(info.register_seconds, 2),
                   "gpu_mem_mapping_bytes": info.gpu_mem_delta,
                   "mapping_ratio": round(cfg.table_bytes / max(info.gpu_mem_delta, 1), 1),
-                  "csr_gen_s": round(csr_s, 2), "total_s": round(time.time() - t_setup, 1), "sms": sm_count},
+                  "csr_gen_s": round(csr_s, 2), "total_s": round(time.time() - t_setup, 1), "sms": sm_count,
+                  "host_numa_nodes": dgz.host_numa_nodes(),
+                  "host_table_policy": "anonymous THP mapping (first touch)" if G == 1 else
+                                       "/dev/shm object shared by the ranks, NUMA-interleaved"},
     }
     fetcher.close()
     if args.csr == "host":

@@ -70,11 +70,16 @@ DGZ_API uint64_t dgz_kernel_launches(void);
                                    (single process; not shareable by name) */
 #define DGZ_HOST_HUGETLB_2M 16u /* anonymous MAP_HUGETLB 2 MiB pages (needs vm.nr_hugepages) */
 #define DGZ_HOST_HUGETLB_1G 32u /* anonymous MAP_HUGETLB 1 GiB pages */
+#define DGZ_HOST_NUMA_INTERLEAVE 64u /* mbind(MPOL_INTERLEAVE) over the online NUMA nodes before first
+                                        touch (a no-op on one node): multi-socket boxes whose G GPUs all
+                                        read the one shared table (SURVEY 7 "host aggregate") */
 #define DGZ_HOST_VMM 4u      /* CUDA VMM host allocation (cuMemCreate on host NUMA node 0): pinned,
                                 CPU-accessible, mapped into the current GPU with large pages at the
                                 same address.  Needs a CUDA device; shm_name must be NULL (share it
                                 across processes with dgz_host_export / dgz_host_import). */
 
+/* Number of online NUMA nodes of the host (1 when unknown). */
+DGZ_API int dgz_host_numa_nodes(void);
 /* Map `bytes` of host memory.  shm_name == NULL: private anonymous mapping.  Otherwise a POSIX
  * shared-memory object (/dev/shm/<name>): create != 0 creates/truncates it to `bytes`,
  * create == 0 opens an existing object of at least `bytes` bytes.  *ptr receives a

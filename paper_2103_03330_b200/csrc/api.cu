@@ -14,6 +14,9 @@
 #include <mutex>
 #include <map>
 
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include "internal.h"
 
 namespace dgz {
@@ -71,6 +74,30 @@ extern "C" uint64_t dgz_kernel_launches(void) { return g_launches.load(); }
 // ---------------------------------------------------------------------------------------------
 // Host table manager
 // ---------------------------------------------------------------------------------------------
+// Online NUMA nodes (/sys/devices/system/node/online, e.g. "0-1" or "0,2-3") as a bit mask.
+static int numa_online_mask(unsigned long* mask, int max_nodes) {
+    FILE* f = fopen("/sys/devices/system/node/online", "r");
+    if (!f) return 1;   // no NUMA information: treat as one node
+    char line[256] = {0};
+    if (!fgets(line, sizeof line, f)) line[0] = 0;
+    fclose(f);
+    int count = 0;
+    for (char* tok = strtok(line, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+        int lo = 0, hi = 0;
+        if (sscanf(tok, "%d-%d", &lo, &hi) < 2) hi = lo = atoi(tok);
+        for (int n = lo; n <= hi && n < max_nodes; ++n) {
+            mask[n / (8 * sizeof(unsigned long))] |= 1ul << (n % (8 * sizeof(unsigned long)));
+            ++count;
+        }
+    }
+    return count > 0 ? count : 1;
+}
+
+extern "C" int dgz_host_numa_nodes(void) {
+    unsigned long mask[16] = {0};
+    return numa_online_mask(mask, 16 * 8 * (int)sizeof(unsigned long));
+}
+
 extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int create, uint32_t flags, void** ptr) {
     DGZ_REQUIRE(ptr && bytes > 0, "dgz_host_alloc: null ptr or zero size");
     *ptr = nullptr;
@@ -122,6 +149,21 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
         close(fd);
     }
     if (p == MAP_FAILED) { set_error("mmap(%zu): %s", bytes, strerror(errno)); return DGZ_ERR_NOMEM; }
+    if (flags & DGZ_HOST_NUMA_INTERLEAVE) {
+        // pages are placed round-robin over the online NUMA nodes at first touch (for a /dev/shm
+        // object this sets the object's shared policy): on a multi-socket box the G ranks' random
+        // reads then spread over every socket's memory controllers instead of the filling rank's
+        const int max_nodes = 1024;
+        unsigned long mask[max_nodes / (8 * sizeof(unsigned long))] = {0};
+        if (numa_online_mask(mask, max_nodes) > 1) {
+            const int mpol_interleave = 3;   // MPOL_INTERLEAVE (linux/mempolicy.h)
+            if (syscall(SYS_mbind, p, bytes, mpol_interleave, mask, (unsigned long)max_nodes, 0u) != 0) {
+                set_error("mbind(MPOL_INTERLEAVE, %zu bytes): %s", bytes, strerror(errno));
+                munmap(p, bytes);
+                return DGZ_ERR_INVALID;
+            }
+        }
+    }
     if (flags & DGZ_HOST_HUGEPAGE) madvise(p, bytes, MADV_HUGEPAGE);
     if (flags & DGZ_HOST_POPULATE) {
         volatile uint8_t* b = (volatile uint8_t*)p;

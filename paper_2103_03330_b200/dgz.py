@@ -25,6 +25,7 @@ OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_RANGE, ERR_STATE = range(6)
 F32, F16, BF16, U8 = range(4)
 REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED, REG_DEVICE = 1, 2, 4, 8, 16
 HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM, HOST_CUDA_PINNED, HOST_HUGETLB_2M, HOST_HUGETLB_1G = 1, 2, 4, 8, 16, 32
+HOST_NUMA_INTERLEAVE = 64
 GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
 SCHED_AUTO, SCHED_INTERLEAVED, SCHED_BLOCKED = range(3)
 FLAG_NO_MERGE, FLAG_DEEP, FLAG_ORDER, FLAG_STREAM_STORES, FLAG_EVICT_FIRST_LOADS = 1, 2, 4, 8, 16
@@ -97,6 +98,7 @@ _SIGS = {
     "dgz_last_error": ([], ctypes.c_char_p),
     "dgz_device_sm_count": ([], ctypes.c_int),
     "dgz_kernel_launches": ([], ctypes.c_uint64),
+    "dgz_host_numa_nodes": ([], ctypes.c_int),
     "dgz_host_alloc": ([ctypes.c_char_p, _sz, ctypes.c_int, _u32, _P(_vp)], ctypes.c_int),
     "dgz_host_free": ([_vp, _sz], ctypes.c_int),
     "dgz_host_unlink": ([ctypes.c_char_p], ctypes.c_int),
@@ -208,6 +210,11 @@ class HostBuffer:
     def unlink(self) -> None:
         if self.shm_name:
             _check(_lib.dgz_host_unlink(self.shm_name.encode()), "dgz_host_unlink")
+
+
+def host_numa_nodes() -> int:
+    """Online NUMA nodes of the host (dgz_host_numa_nodes)."""
+    return int(_lib.dgz_host_numa_nodes())
 
 
 def host_unlink(shm_name: str) -> None:

@@ -66,3 +66,23 @@ def test_host_table_manager_shared_mapping():
     finally:
         a.unlink()
         a.free()
+
+
+def test_numa_interleaved_host_allocation():
+    """DGZ_HOST_NUMA_INTERLEAVE: anonymous and /dev/shm mappings are created (interleaved over the
+    online nodes on a multi-socket host, unchanged on one node) and are ordinary memory."""
+    import numpy as np
+    from paper_2103_03330_b200 import dgz
+    assert dgz.host_numa_nodes() >= 1
+    a = dgz.HostBuffer(8 << 20, flags=dgz.HOST_NUMA_INTERLEAVE | dgz.HOST_HUGEPAGE)
+    name = f"/dgz_numa_test_{os.getpid()}"
+    b = dgz.HostBuffer(4 << 20, name, create=True, flags=dgz.HOST_NUMA_INTERLEAVE)
+    try:
+        for buf in (a, b):
+            v = buf.numpy()
+            v[::4096] = 7
+            assert int(v[::4096].sum()) == 7 * v[::4096].size and int(v[1::4096].sum()) == 0
+    finally:
+        a.free()
+        b.unlink()
+        b.free()
