@@ -560,12 +560,16 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
     rows = [{"partition": "none (whole GPU, high-priority fetch stream)", "fetch_sms": 148, "t_fetch_ms": round(t_g0, 3),
              "t_consumer_ms": round(t_c0, 3), "t_step_overlapped_ms": round(t_o0, 3),
              "exposed_fetch_ms": round(max(0.0, t_o0 - t_c0), 3)}]
-    for k in (4, 8, 16, 32):
+    # partition shapes: k SMs spread over every GPC, or k contiguous SMs of the split (DESIGN 5:
+    # the gather's rate depends strongly and reproducibly on WHICH SMs it gets, explore25)
+    for k, pflags in ((8, dgz.PARTITION_SPREAD), (16, dgz.PARTITION_SPREAD), (24, dgz.PARTITION_SPREAD),
+                      (8, 0), (16, 0), (24, 0)):
         try:
-            part = dgz.Partition(k, -1, dgz.PARTITION_SPREAD)
+            part = dgz.Partition(k, -1, pflags)
         except Exception as e:  # green contexts unavailable: report and skip
             rows.append({"fetch_sms": k, "error": str(e)[:200]})
             continue
+        shape = "spread over the GPCs" if pflags else "contiguous"
         # grid sized to the partition: one 8-warp CTA per SM, 16 line loads per lane (explore15)
         pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
         # sampler placement: in front of the gather on the small partition, or in the consumer's stream
@@ -575,7 +579,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
             f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream,
                                  gather_cfg=pcfg, sample_stream=part.compute_stream if where == "consumer stream" else None)
             t_g, t_c, t_o, _ = measure(f, part.compute_stream, repeat=repeat)
-            rows.append({"partition": f"green context, sampler in the {where}", "fetch_sms": part.fetch_sms,
+            rows.append({"partition": f"green context ({shape}), sampler in the {where}", "fetch_sms": part.fetch_sms,
                          "compute_sms": part.compute_sms,
                          "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
                          "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
