@@ -344,6 +344,14 @@ typedef struct dgz_partition_s* dgz_partition;
 #define DGZ_PARTITION_FINE 1u   /* CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING: finer SM counts */
 #define DGZ_PARTITION_SPREAD 2u /* fetch SMs taken evenly across the device (all GPCs) from the
                                    finest split; the compute group gets every other SM */
+/* Explicit SM sets: the device's SMs as the smallest groups a green-context split allows (in the
+ * driver's order; *sms_per_group SMs each), and a partition whose fetch side is exactly the listed
+ * groups (the compute side gets the rest).  Which SMs a translation-bound gather runs on changes
+ * its rate at a fixed SM count; these entry points let a caller measure and
+ * pick them. */
+DGZ_API dgz_status dgz_partition_group_count(int32_t* n_groups, int32_t* sms_per_group);
+DGZ_API dgz_status dgz_partition_create_groups(const int32_t* fetch_groups, int32_t n_fetch_groups, int32_t fetch_priority,
+                                               dgz_partition* out);
 DGZ_API dgz_status dgz_partition_create(int32_t fetch_sms, int32_t fetch_priority, uint32_t flags, dgz_partition* out);
 DGZ_API dgz_status dgz_partition_get(dgz_partition p, dgz_stream* fetch_stream, dgz_stream* compute_stream,
                                      int32_t* fetch_sms, int32_t* compute_sms);

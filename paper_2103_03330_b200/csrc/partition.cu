@@ -146,6 +146,80 @@ extern "C" dgz_status dgz_partition_create(int32_t fetch_sms, int32_t fetch_prio
     return DGZ_OK;
 }
 
+// The device's SMs as the smallest groups a green-context split allows (in the driver's order).
+static dgz_status min_groups(CUdevice* cd, std::vector<CUdevResource>& groups, CUdevResource* rem) {
+    int dev = 0;
+    DGZ_CUDA(cudaGetDevice(&dev));
+    DGZ_CUDA(cudaFree(nullptr));
+    CUresult r = gdrv().device_get(cd, dev);
+    if (r != CUDA_SUCCESS) return gfail(r, "cuDeviceGet");
+    CUdevResource all;
+    r = gdrv().get_resource(*cd, &all, CU_DEV_RESOURCE_TYPE_SM);
+    if (r != CUDA_SUCCESS) return gfail(r, "cuDeviceGetDevResource");
+    const unsigned use = CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
+    unsigned int ng = 0;
+    r = gdrv().split(nullptr, &ng, &all, nullptr, use, 1);
+    if (r != CUDA_SUCCESS || ng == 0) return gfail(r, "cuDevSmResourceSplitByCount(query)");
+    groups.resize(ng);
+    r = gdrv().split(groups.data(), &ng, &all, rem, use, 1);
+    if (r != CUDA_SUCCESS) return gfail(r, "cuDevSmResourceSplitByCount");
+    groups.resize(ng);
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_partition_group_count(int32_t* n_groups, int32_t* sms_per_group) {
+    DGZ_REQUIRE(n_groups && sms_per_group, "dgz_partition_group_count: null argument");
+    if (!gdrv().ok) { set_error("green-context driver entry points unavailable"); return DGZ_ERR_CUDA; }
+    CUdevice cd;
+    std::vector<CUdevResource> groups;
+    CUdevResource rem;
+    dgz_status st = min_groups(&cd, groups, &rem);
+    if (st != DGZ_OK) return st;
+    *n_groups = (int32_t)groups.size();
+    *sms_per_group = groups.empty() ? 0 : (int32_t)groups[0].sm.smCount;
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_partition_create_groups(const int32_t* fetch_groups, int32_t n_fetch_groups, int32_t fetch_priority,
+                                                  dgz_partition* out) {
+    DGZ_REQUIRE(out && fetch_groups && n_fetch_groups > 0, "dgz_partition_create_groups: bad arguments");
+    *out = nullptr;
+    if (!gdrv().ok) { set_error("green-context driver entry points unavailable"); return DGZ_ERR_CUDA; }
+    CUdevice cd;
+    std::vector<CUdevResource> groups;
+    CUdevResource rem;
+    dgz_status st = min_groups(&cd, groups, &rem);
+    if (st != DGZ_OK) return st;
+    const int ng = (int)groups.size();
+    std::vector<char> pick(ng, 0);
+    for (int i = 0; i < n_fetch_groups; ++i) {
+        DGZ_REQUIRE(fetch_groups[i] >= 0 && fetch_groups[i] < ng && !pick[fetch_groups[i]],
+                    "dgz_partition_create_groups: group %d invalid or repeated (%d groups)", fetch_groups[i], ng);
+        pick[fetch_groups[i]] = 1;
+    }
+    DGZ_REQUIRE(n_fetch_groups < ng || rem.sm.smCount > 0, "dgz_partition_create_groups: nothing left for compute");
+    dgz_partition p = new dgz_partition_s();
+    std::vector<CUdevResource> sel[2];
+    for (int i = 0; i < ng; ++i) sel[pick[i] ? 0 : 1].push_back(groups[i]);
+    if (rem.sm.smCount) sel[1].push_back(rem);
+    for (int i = 0; i < 2; ++i) {
+        CUdevResourceDesc desc;
+        CUresult r = gdrv().gen_desc(&desc, sel[i].data(), (unsigned)sel[i].size());
+        if (r == CUDA_SUCCESS) r = gdrv().create(&p->g[i], desc, cd, CU_GREEN_CTX_DEFAULT_STREAM);
+        if (r == CUDA_SUCCESS) r = gdrv().stream_create(&p->s[i], p->g[i], CU_STREAM_NON_BLOCKING, i == 0 ? fetch_priority : 0);
+        if (r != CUDA_SUCCESS) {
+            dgz_status e = gfail(r, "green context creation");
+            dgz_partition_destroy(p);
+            return e;
+        }
+        int c = 0;
+        for (auto& g : sel[i]) c += (int)g.sm.smCount;
+        p->sms[i] = c;
+    }
+    *out = p;
+    return DGZ_OK;
+}
+
 extern "C" dgz_status dgz_partition_get(dgz_partition p, dgz_stream* fetch_stream, dgz_stream* compute_stream, int32_t* fetch_sms,
                                         int32_t* compute_sms) {
     DGZ_REQUIRE(p, "dgz_partition_get: null partition");

@@ -130,6 +130,8 @@ _SIGS = {
     "dgz_aggregate_mean": ([_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp], ctypes.c_int),
     "dgz_partition_create": ([_i32, _i32, _u32, _P(_vp)], ctypes.c_int),
     "dgz_partition_get": ([_vp, _P(_vp), _P(_vp), _P(_i32), _P(_i32)], ctypes.c_int),
+    "dgz_partition_group_count": ([_P(_i32), _P(_i32)], ctypes.c_int),
+    "dgz_partition_create_groups": ([_P(_i32), _i32, _i32, _P(_vp)], ctypes.c_int),
     "dgz_partition_destroy": ([_vp], ctypes.c_int),
     "dgz_probe_stream": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
@@ -566,9 +568,14 @@ class Partition:
     """Fetch / compute SM groups with one stream each (dgz_partition_*); streams are exposed as
     torch.cuda.ExternalStream so PyTorch work can be queued on the compute group."""
 
-    def __init__(self, fetch_sms: int, fetch_priority: int = -1, flags: int = 0):
+    def __init__(self, fetch_sms: int, fetch_priority: int = -1, flags: int = 0, groups=None):
         h = _vp()
-        _check(_lib.dgz_partition_create(fetch_sms, fetch_priority, flags, ctypes.byref(h)), "dgz_partition_create")
+        if groups is not None:     # explicit SM groups (dgz_partition_create_groups)
+            arr = (ctypes.c_int32 * len(groups))(*groups)
+            _check(_lib.dgz_partition_create_groups(arr, len(groups), fetch_priority, ctypes.byref(h)),
+                   "dgz_partition_create_groups")
+        else:
+            _check(_lib.dgz_partition_create(fetch_sms, fetch_priority, flags, ctypes.byref(h)), "dgz_partition_create")
         self.handle = h.value
         fs, cs, fn, cn = _vp(), _vp(), _i32(), _i32()
         _check(_lib.dgz_partition_get(self.handle, ctypes.byref(fs), ctypes.byref(cs), ctypes.byref(fn), ctypes.byref(cn)),
@@ -582,6 +589,13 @@ class Partition:
             torch.cuda.synchronize()
             _check(_lib.dgz_partition_destroy(self.handle), "dgz_partition_destroy")
             self.handle = None
+
+
+def partition_groups() -> tuple:
+    """(number of minimal SM groups, SMs per group) of the current device (dgz_partition_group_count)."""
+    n, per = _i32(), _i32()
+    _check(_lib.dgz_partition_group_count(ctypes.byref(n), ctypes.byref(per)), "dgz_partition_group_count")
+    return n.value, per.value
 
 
 # --- stand-in consumer, probes -------------------------------------------------------------------

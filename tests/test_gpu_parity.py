@@ -353,9 +353,14 @@ def test_fetch_on_green_context_partition(dev):
     t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
     try:
         g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
-        for flags in (dgz.PARTITION_SPREAD, dgz.PARTITION_FINE, 0):
-            part = dgz.Partition(8, -1, flags)
+        ng, per = dgz.partition_groups()
+        assert ng * per <= 148 and per >= 1
+        for flags, groups in ((dgz.PARTITION_SPREAD, None), (dgz.PARTITION_FINE, None), (0, None),
+                              (0, [ng - 1, 3, 7, 20]), (0, list(range(10, 18)))):   # explicit SM groups
+            part = dgz.Partition(8, -1, flags, groups=groups)
             assert part.fetch_sms >= 8 and part.fetch_sms + part.compute_sms <= 148
+            if groups is not None:
+                assert part.fetch_sms == len(groups) * per
             f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, fetch_stream=part.fetch_stream)
             for j in (0, 3):
                 seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
