@@ -502,25 +502,40 @@ class Graph:
 class HostGraph:
     """CSR left in pinned, mapped host memory and read by the sampler with zero-copy loads
     (a graph whose CSR does not fit HBM is sampled where it lies, the way the
-    paper's unified tensor leaves features in host memory).  The offsets and column
-    arrays are registered like feature tables (dgz_register_table as byte tables: pin + map) and
-    the sampler is given their device pointers through the same dgz_csr -- no other change on the
-    path.  ``offsets`` / ``cols`` are host addresses (ints) of int64 [n_nodes + 1] and int32/int64
+    paper's unified tensor leaves features in host memory).  The column array (and with
+    ``offsets_in_hbm=False`` the offsets too) is registered like a feature table (dgz_register_table
+    as a byte table: pin + map) and the sampler is given the device pointers through the same
+    dgz_csr -- no other change on the path.  By default the offsets (8 B per node, a small fraction
+    of the columns) are copied to HBM, so the sampler's host page walks are for columns only.
+    ``offsets`` / ``cols`` are host addresses (ints) of int64 [n_nodes + 1] and int32/int64
     [n_edges] arrays the caller keeps alive, or numpy arrays (copied into HostBuffers here)."""
 
     def __init__(self, offsets, cols, n_nodes: int | None = None, n_edges: int | None = None,
-                 cols_is64: bool | None = None, flags: int = REG_READONLY):
+                 cols_is64: bool | None = None, flags: int = REG_READONLY, offsets_in_hbm: bool = True):
         import numpy as np
         self._owned = []
+        self.offsets_dev = None
         if isinstance(offsets, np.ndarray):
             assert offsets.dtype == np.int64 and cols.dtype in (np.int32, np.int64)
             n_nodes, n_edges, cols_is64 = offsets.size - 1, cols.size, cols.dtype == np.int64
-            offsets, cols = self._copy_in(offsets), self._copy_in(cols) if cols.size else 0
+            if offsets_in_hbm:
+                self.offsets_dev = torch.from_numpy(offsets).cuda()
+                offsets = 0
+            else:
+                offsets = self._copy_in(offsets)
+            cols = self._copy_in(cols) if cols.size else 0
+        elif offsets_in_hbm:
+            import numpy as np
+            hv = (ctypes.c_int64 * (int(n_nodes) + 1)).from_address(int(offsets))
+            self.offsets_dev = torch.from_numpy(np.frombuffer(hv, dtype=np.int64)).cuda()
         assert n_nodes is not None and n_edges is not None and cols_is64 is not None
         self.n_nodes, self.n_edges, self.cols_is64 = int(n_nodes), int(n_edges), bool(cols_is64)
         self.off_table = self.col_table = None
         try:
-            self.off_table = register_table(int(offsets), (self.n_nodes + 1) * 8, 1, U8, flags)
+            # offsets (8 B per node) go to HBM by default -- the columns (8-16x larger on real
+            # graphs) are what does not fit; the sampler then walks host pages only for columns
+            if not offsets_in_hbm:
+                self.off_table = register_table(int(offsets), (self.n_nodes + 1) * 8, 1, U8, flags)
             col_dev = 0
             if self.n_edges:
                 self.col_table = register_table(int(cols), self.n_edges * (8 if cols_is64 else 4), 1, U8, flags)
@@ -528,7 +543,8 @@ class HostGraph:
         except Exception:
             self.close()
             raise
-        self.struct = Csr(self.n_nodes, self.off_table.info.dev_ptr, col_dev, int(self.cols_is64), 0)
+        off_dev = self.offsets_dev.data_ptr() if self.offsets_dev is not None else self.off_table.info.dev_ptr
+        self.struct = Csr(self.n_nodes, off_dev, col_dev, int(self.cols_is64), 0)
 
     def _copy_in(self, a) -> int:
         import numpy as np
@@ -542,6 +558,7 @@ class HostGraph:
             if t is not None:
                 t.unregister()
         self.col_table = self.off_table = None
+        self.offsets_dev = None
         for hb in self._owned:
             hb.free()
         self._owned = []

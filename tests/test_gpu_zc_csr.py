@@ -22,9 +22,9 @@ def dev():
     return torch.device("cuda", 0)
 
 
-def _compare(off, col, seeds, fanouts, rs):
+def _compare(off, col, seeds, fanouts, rs, offsets_in_hbm=True):
     want = oracle.sample_uniform(off, col, seeds, fanouts, rs)
-    g = dgz.HostGraph(off, col)
+    g = dgz.HostGraph(off, col, offsets_in_hbm=offsets_in_hbm)
     try:
         bufs = dgz.SampleBuffers(g.n_nodes, max(len(seeds), 1), fanouts)
         dgz.sample_uniform(g, torch.from_numpy(np.asarray(seeds, dtype=np.int64)).cuda(), fanouts, rs, bufs)
@@ -49,16 +49,17 @@ def test_zero_copy_csr_sampler(dev, n, deg, fan, col64):
     off, col = gen.gen_csr(n, deg, n + 1)
     if col64:
         col = col.astype(np.int64)
-    for j in (0, 5):
+    for j, in_hbm in ((0, True), (5, False)):      # offsets in HBM (default) or also on the host
         seeds = gen.batch_seeds(n, min(1024, n // 2), n + 1, j)
-        _compare(off, col, seeds, fan, gen.batch_rng_seed(n + 1, j))
+        _compare(off, col, seeds, fan, gen.batch_rng_seed(n + 1, j), offsets_in_hbm=in_hbm)
 
 
 def test_zero_copy_csr_edge_cases(dev):
     off = np.zeros(4001, dtype=np.int64)                     # no edges at all: cols may be NULL
-    _compare(off, np.zeros(0, dtype=np.int32), [5, 17, 3999, 5], (3, 2), 9)
+    for in_hbm in (True, False):
+        _compare(off, np.zeros(0, dtype=np.int32), [5, 17, 3999, 5], (3, 2), 9, in_hbm)
     off, col = gen.gen_csr(3000, 6.0, 5)
-    _compare(off, col, [7, 3, 7, 9, 3, 2999, 0], (4, 3), 99)
+    _compare(off, col, [7, 3, 7, 9, 3, 2999, 0], (4, 3), 99, False)
 
 
 def test_zero_copy_csr_fetch_config3(dev):

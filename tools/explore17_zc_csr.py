@@ -17,7 +17,8 @@ for cid in (3, 4):
     c = gen.CONFIGS[cid]
     off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
     graphs = {"hbm": dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda()),
-              "host": dgz.HostGraph(off, col)}
+              "host cols (offsets in HBM)": dgz.HostGraph(off, col),
+              "host cols + offsets": dgz.HostGraph(off, col, offsets_in_hbm=False)}
     bufs = dgz.SampleBuffers(c.n_nodes, c.batch, c.fanouts)
     seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in range(24)]
     rs = [gen.batch_rng_seed(c.seed, j) for j in range(24)]
@@ -40,5 +41,6 @@ for cid in (3, 4):
                               "rows": int(bufs.sizes_host[-1])}), flush=True)
     torch.cuda.synchronize()
     part.destroy()
-    graphs["host"].close()
+    for k in list(graphs)[1:]:
+        graphs[k].close()
     del graphs, bufs
