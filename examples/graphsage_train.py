@@ -169,10 +169,11 @@ def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
         e.record()
     t_cpu = []
 
-    def produce(q, lo, hi):
+    def produce(q, slots, lo, hi):
         for i in range(lo, hi):
-            p = i % 2
-            free[p].synchronize()                       # slot p's previous training step is done
+            p = slots.get()                             # the main thread has enqueued slot p's last training step
+            assert p == i % 2
+            free[p].synchronize()                       # ... and that step has finished on the GPU
             b = bufs[p]
             with torch.cuda.stream(s_fetch):
                 dgz.sample_uniform(graph, seeds[i], c.fanouts, rng[i], b, stream=s_fetch)
@@ -189,7 +190,10 @@ def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
 
     def loop(lo, hi):
         q = queue.Queue(maxsize=1)
-        th = threading.Thread(target=produce, args=(q, lo, hi), daemon=True)
+        slots = queue.Queue()                           # slot tokens: a slot is re-filled only after its
+        slots.put(lo % 2)                               # training step was enqueued (free[p] recorded)
+        slots.put((lo + 1) % 2)
+        th = threading.Thread(target=produce, args=(q, slots, lo, hi), daemon=True)
         th.start()
         loss = None
         while True:
@@ -201,6 +205,7 @@ def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
             cur.wait_event(ready[p])
             loss = trainer.step(rows[p], bufs[p], sz)
             free[p].record(cur)
+            slots.put(p)
         th.join()
         return loss.detach()
     loop(0, 2)

@@ -6,7 +6,7 @@ width over the 56.9 GB buffer (base offset 0 and 4), useful GB/s (GB = 1e9).
   dma : torch.index_select with all host threads into pinned staging, 32 MiB chunks, each chunk's
         cudaMemcpyAsync H2D overlapping the CPU gather of the next (double-buffered)
 
-    python tools/sweep_dma_vs_zc.py > gpurun_out/sweep_dma_vs_zc.jsonl
+    python tools/sweep_dma_vs_zc.py [--zc-only] [--widths=66,202,...] > gpurun_out/sweep_dma_vs_zc.jsonl
 """
 import json
 import os
@@ -50,7 +50,11 @@ def dma_gather(host_rows, ids_cpu, R):
     cs.synchronize()
 
 
-for R in gen.SWEEP_ROW_BYTES:
+WIDTHS = gen.SWEEP_ROW_BYTES
+for a in sys.argv[1:]:
+    if a.startswith("--widths="):          # e.g. --widths=66,202,1030 (fp16 rows with odd dims: 2 B aligned)
+        WIDTHS = tuple(int(x) for x in a.split("=", 1)[1].split(","))
+for R in WIDTHS:
     for base in (0, 4):
         rows = (total - base) // R
         n = min(rows, (256 << 20) // R)
