@@ -1,4 +1,4 @@
-"""compute-sanitizer target for the session-2 features (tools/sanitize_s2.sh): zero-copy CSR
+"""compute-sanitizer target (test infrastructure: it checks against the oracle) for the session-2 features (tools/sanitize_s2.sh): zero-copy CSR
 sampling, the sorted gather's default launch shapes, cache hints, local-shard cache fill + cached
 gather, order_ids -- each checked against the oracle so a silent corruption also fails."""
 import os
@@ -7,7 +7,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import dgz_inputs as gen  # noqa: E402
 import oracle  # noqa: E402
 from paper_2103_03330_b200 import dgz  # noqa: E402
