@@ -98,12 +98,18 @@ def timed(fn, K):
     return (time.perf_counter() - t0) * 1e3 / K, r
 
 
-def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute", spread=False):
+def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute", spread=False,
+                     tune=False):
     """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
     sampler (HBM-bound, 0.35 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
-    part = dgz.Partition(fetch_sms, -1, dgz.PARTITION_SPREAD if spread else 0)
-    pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
+    tuned = None
+    if tune:   # measure a few partition shapes on this chip and keep the fastest (pipeline.tune_fetch_partition)
+        from paper_2103_03330_b200.pipeline import tune_fetch_partition
+        part, pcfg, tuned = tune_fetch_partition(table, graph, c.fanouts, c.batch, seeds[:4], rng[:4])
+    else:
+        part = dgz.Partition(fetch_sms, -1, dgz.PARTITION_SPREAD if spread else 0)
+        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
     comp = part.compute_stream
     f = MinibatchFetcher(table, graph, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=pcfg,
                          sample_stream=comp if sample_on == "compute" else None)
@@ -142,7 +148,7 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
     out = {"step_ms": round(t_pipe, 3), "fetch_alone_ms": round(t_fetch, 3), "train_alone_ms": round(t_train, 3),
            "exposed_fetch_ms": round(max(0.0, t_pipe - t_train), 3), "loss": round(float(loss), 4),
            "fetch_sms": part.fetch_sms, "train_sms": part.compute_sms, "sampler_on": sample_on,
-           "fetch_partition": "spread over the GPCs" if spread else "contiguous",
+           "fetch_partition": ("tuned: " + json.dumps(tuned)) if tuned else ("spread over the GPCs" if spread else "contiguous"),
            "rows_per_minibatch": sz[-1]}
     f.close()
     torch.cuda.synchronize()
@@ -239,6 +245,7 @@ def main():
     ap.add_argument("--fetch-sms", type=int, default=16)
     ap.add_argument("--sample-on", default="compute", choices=["compute", "fetch"])
     ap.add_argument("--spread", action="store_true", help="fetch SMs spread over the GPCs (default: contiguous)")
+    ap.add_argument("--tune", action="store_true", help="time a few fetch partitions first and keep the fastest")
     ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))   # one core left for the training loop
     a = ap.parse_args()
     # one process per GPU under torchrun (DDP; DGZ_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 with gloo)
@@ -282,7 +289,7 @@ def main():
     threads = max(1, a.threads // G)
     if "zc" in modes:
         res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms,
-                                     lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread)
+                                     lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune)
     if "dma" in modes:
         host_rows = torch.from_numpy(buf.numpy(0, c.table_bytes)).view(c.n_nodes, c.row_bytes)
         res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, Trainer(c, a.hidden, a.classes, G > 1))
@@ -291,7 +298,7 @@ def main():
         dev.copy_(torch.from_numpy(buf.numpy(0, c.table_bytes)))
         dtab = dgz.DeviceTable(dev.data_ptr(), c.n_nodes, c.dim, dgz.F32)
         res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms,
-                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread)
+                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune)
         dtab.unregister()
         del dev
     if G > 1:   # per-rank results to rank 0; the job's step time is the slowest rank's

@@ -203,3 +203,51 @@ def _as_i64(x: int) -> int:
     """uint64 sampler seed -> the int64 with the same bits (torch tensors are signed)."""
     x &= (1 << 64) - 1
     return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds, rng_seeds, candidates=None,
+                         warps_per_cta: int = 8):
+    """Pick the green-context partition whose SMs gather fastest on THIS chip (DESIGN.md section 5:
+    at a fixed SM count the zero-copy gather's rate depends strongly and reproducibly on which SMs
+    walk the GPU page tables, and the best set differs between chips).  Samples the given minibatches
+    once, then times the address-sorted gather of all of them on each candidate partition (alone)
+    and returns (best dgz.Partition, its gather config, [(candidate, GB/s), ...]); the other
+    partitions are destroyed.  candidates: list of dicts with either {"sms": k, "flags": f} or
+    {"groups": [...]} (dgz_partition_create_groups); default: 16 and 24 SMs, contiguous and spread."""
+    if candidates is None:
+        candidates = [{"sms": 16, "flags": 0}, {"sms": 16, "flags": dgz.PARTITION_SPREAD},
+                      {"sms": 24, "flags": 0}, {"sms": 24, "flags": dgz.PARTITION_SPREAD}]
+    fanouts = tuple(int(f) for f in fanouts)
+    L = len(fanouts)
+    bufs = []
+    for s, r in zip(seeds, rng_seeds):
+        b = dgz.SampleBuffers(graph.n_nodes, max_seeds, fanouts, blocks=False, local=False)
+        dgz.sample_uniform(graph, s, fanouts, r, b)
+        bufs.append(b)
+    torch.cuda.synchronize()
+    nbytes = sum(int(b.sizes_host[-1]) for b in bufs) * table.row_bytes
+    out = torch.empty(max(b.bounds[-1] for b in bufs) * table.row_bytes, dtype=torch.uint8, device="cuda")
+    results, best = [], None
+    for cand in candidates:
+        part = dgz.Partition(cand.get("sms", 0), -1, cand.get("flags", 0), groups=cand.get("groups"))
+        cfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=warps_per_cta, flags=dgz.FLAG_DEEP)
+        s = part.fetch_stream
+        b0 = bufs[0]
+        dgz.gather_perm(table, b0.ids_sorted, b0.ids_sorted_pos, out, n=b0.bounds[-1], n_dev=b0.sizes_dev[L:L + 1],
+                        cfg=cfg, stream=s)                       # warm-up
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for b in bufs:
+            dgz.gather_perm(table, b.ids_sorted, b.ids_sorted_pos, out, n=b.bounds[-1], n_dev=b.sizes_dev[L:L + 1],
+                            cfg=cfg, stream=s)
+        e.record(s)
+        e.synchronize()
+        gbs = nbytes / (a.elapsed_time(e) * 1e-3) / 1e9
+        results.append((dict(cand, fetch_sms=part.fetch_sms), round(gbs, 2)))
+        if best is None or gbs > best[2]:
+            if best is not None:
+                best[0].destroy()
+            best = (part, cfg, gbs)
+        else:
+            part.destroy()
+    return best[0], best[1], results

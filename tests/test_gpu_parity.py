@@ -595,3 +595,33 @@ def test_gather_perm_default_launch_shapes(dev, R, rows, n):
         dgz.check_errors(t.table)
     finally:
         t.close()
+
+
+def test_tune_fetch_partition_then_fetch(dev):
+    """pipeline.tune_fetch_partition times candidate partitions and returns the fastest; a fetch on
+    it is byte-identical to the oracle."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher, tune_fetch_partition
+    c = gen.CONFIGS[1]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+        seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in range(2)]
+        rs = [gen.batch_rng_seed(c.seed, j) for j in range(2)]
+        ng, per = dgz.partition_groups()
+        cands = [{"sms": 8, "flags": dgz.PARTITION_SPREAD}, {"groups": list(range(0, 8))}]
+        part, cfg, res = tune_fetch_partition(t.table, g, c.fanouts, c.batch, seeds, rs, candidates=cands)
+        assert len(res) == 2 and all(gbs > 0 for _, gbs in res)
+        assert part.fetch_sms in (r[0]["fetch_sms"] for r in res)
+        f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=cfg)
+        seeds_np = gen.batch_seeds(c.n_nodes, c.batch, c.seed, 5)
+        mb = f.fetch(torch.from_numpy(seeds_np).cuda(), gen.batch_rng_seed(c.seed, 5))
+        n = mb.sizes()[-1]
+        want = oracle.sample_uniform(off, col, seeds_np, c.fanouts, gen.batch_rng_seed(c.seed, 5), with_blocks=False)
+        exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+        assert np.array_equal(mb.bufs.ids[:n].cpu().numpy(), want.U)
+        assert np.array_equal(mb.rows[:n].cpu().numpy(), exp)
+        del f
+        part.destroy()
+    finally:
+        t.close()
