@@ -305,7 +305,9 @@ def run_ours(args, d: Dist):
     seeds_dev = [x.cuda() for x in seeds_host]
     rng = [gen.batch_rng_seed(cfg.seed, j) for j in batches]
 
-    gcfg = dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps) if (args.gather_sms or args.gather_warps) else None
+    gflags = dgz.FLAG_DYNAMIC if args.dynamic else 0
+    gcfg = (dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps, flags=gflags)
+            if (args.gather_sms or args.gather_warps or gflags) else None)
     sm_count_all = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True,
                                sampler_sms=args.sampler_sms, graphs=args.graphs)
@@ -388,6 +390,7 @@ def run_ours(args, d: Dist):
                    "pipeline": fetcher.mode,
                    "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else "pinned host memory, sampled by zero-copy",
                    "gather": {"variant": "segment", "sm_count": args.gather_sms or sm_count_all,
+                              "schedule": "work counter" if args.dynamic else "static interleave",
                               "warps_per_cta": args.gather_warps or 2, "lines_in_flight_per_warp": 64,
                               "order": "address-sorted + inverse permutation"}},
         "per_gpu_gbs": round(per_gpu, 3),
@@ -571,7 +574,8 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
             continue
         shape = "spread over the GPCs" if pflags else "contiguous"
         # grid sized to the partition: one 8-warp CTA per SM, 16 line loads per lane (explore15)
-        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP)
+        # work-counter batches: a partition's slower SMs take fewer batches (explore28)
+        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
         # sampler placement: in front of the gather on the small partition, or in the consumer's stream
         # between consumer steps (its full-partition bitmap passes then run beside the gather and slow
         # its page walks, but it leaves the small partition; DESIGN 5) -- both measured
@@ -727,6 +731,7 @@ def main():
     ap.add_argument("--graphs", action="store_true", help="replay sampler + gather as one CUDA graph per slot")
     ap.add_argument("--csr", default="hbm", choices=["hbm", "host"],
                     help="CSR replicated in HBM (default) or left in pinned host memory and sampled by zero-copy")
+    ap.add_argument("--dynamic", action="store_true", help="gather batches from a work counter (DGZ_GATHER_FLAG_DYNAMIC)")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false")
     args = ap.parse_args()

@@ -182,6 +182,8 @@ typedef struct {
                                             device, gather, scatter back); same result */
 #define DGZ_GATHER_FLAG_STREAM_STORES 8  /* SEGMENT: HBM stores as st.global.cs (evict-first in L2) */
 #define DGZ_GATHER_FLAG_EVICT_FIRST_LOADS 16 /* SEGMENT: zero-copy loads under an L2 evict_first policy */
+#define DGZ_GATHER_FLAG_DYNAMIC 32       /* SEGMENT: warps take 32-row batches from a work counter (in
+                                            ascending order) instead of a static interleave */
 
 /* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
  * gathers min(*n_dev, n) rows (n is the capacity), so a gather can follow the sampler on the

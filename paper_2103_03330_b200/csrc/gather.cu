@@ -99,7 +99,8 @@ template <int SW, int U, bool MERGE, bool CACHED, typename IdxT>
 __global__ void __launch_bounds__(512, 1)
 gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, const IdxT* __restrict__ idx,
                       const int64_t* __restrict__ dst_pos, int64_t n_cap, const int64_t* __restrict__ n_dev,
-                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked, const CacheArgs ca, int hints) {
+                      uint8_t* __restrict__ dst, int* __restrict__ err, int blocked, const CacheArgs ca, int hints,
+                      unsigned long long* __restrict__ ctr) {
     int64_t n = n_cap;
     if (n_dev) {
         const int64_t m = *n_dev;
@@ -150,11 +151,32 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
         if constexpr (CACHED) return (id >= 0 && id < rows) ? ca.slot[id] : -1;
         return -1;
     };
-    int64_t id_n1 = load_id(bcur), id_n2 = load_id(bcur + bstep);
+    // Batch order: static (warp w takes w, w + W, ...) or, with a work counter (ctr != nullptr,
+    // DGZ_GATHER_FLAG_DYNAMIC), grabbed in ascending order by whichever warp is free -- the sorted
+    // list is still swept as one narrow window, and warps on SMs that walk the page tables faster
+    // take more batches instead of every warp waiting for the slowest SM at the end.
+    const bool dyn = ctr != nullptr && !blocked;
+    auto grab = [&]() -> int64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(ctr, 1ull);
+        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+    };
+    int64_t bn1, bn2;   // the next two batches of this warp (index loads run ahead on them)
+    if (dyn) {
+        bcur = grab();
+        bn1 = grab();
+        bn2 = grab();
+    } else {
+        bn1 = bcur + bstep;
+        bn2 = bcur + 2 * bstep;
+    }
+    int64_t id_n1 = load_id(bcur), id_n2 = load_id(bn1);
     int64_t dp_n1 = load_dp(bcur);
     int32_t sl_n1 = load_slot(id_n1);
 
-    for (; bcur < bend; bcur += bstep) {
+    unsigned long long pend = 0;   // lane 0's grab for the batch after bn2, in flight during this batch
+    for (; bcur < bend; bcur = bn1, bn1 = bn2, bn2 = dyn ? (int64_t)__shfl_sync(0xffffffffu, pend, 0) : bn2 + bstep) {
+        if (dyn && lane == 0) pend = atomicAdd(ctr, 1ull);   // consumed only at the loop's end: no stall
         const int64_t b0 = bcur << 5;
         const int64_t r = b0 + lane;
         int64_t id = id_n1;
@@ -162,8 +184,8 @@ gather_segment_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, 
         const int32_t slot = sl_n1;
         id_n1 = id_n2;
         sl_n1 = load_slot(id_n1);
-        dp_n1 = load_dp(bcur + bstep);
-        id_n2 = load_id(bcur + 2 * bstep);
+        dp_n1 = load_dp(bn1);
+        id_n2 = load_id(bn2);
         if (r < n && (id < 0 || id >= rows)) {
             atomicOr(err, 1);
             id = -1;
@@ -301,6 +323,7 @@ struct SegLaunch {
     int* err;
     int blocks, threads, blocked;
     cudaStream_t s;
+    unsigned long long* ctr;   // zeroed work counter (DGZ_GATHER_FLAG_DYNAMIC) or nullptr
 };
 
 inline int hints_of(int flags) {
@@ -311,10 +334,12 @@ template <int SW, int U, bool MERGE, typename IdxT>
 void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
     if (L.cache) {
         gather_segment_kernel<SW, U, MERGE, true, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
-            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache, hints_of(L.flags));
+            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache, hints_of(L.flags),
+            L.ctr);
     } else {
         gather_segment_kernel<SW, U, MERGE, false, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
-            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, CacheArgs{}, hints_of(L.flags));
+            t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, CacheArgs{}, hints_of(L.flags),
+            L.ctr);
     }
     dgz::count_launch();
 }
@@ -408,7 +433,8 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
                                                 : (variant == DGZ_GATHER_BULK ? 8 : ((sorted_path && !hbm_table) ? 2 : 16));
     int flags = cfg ? cfg->flags : 0;
     if (sorted_path && !hbm_table && !bounded && !(cfg && cfg->warps_per_cta > 0) &&
-        (flags & ~(DGZ_GATHER_FLAG_NO_MERGE | DGZ_GATHER_FLAG_STREAM_STORES | DGZ_GATHER_FLAG_EVICT_FIRST_LOADS)) == 0) {
+        (flags & ~(DGZ_GATHER_FLAG_NO_MERGE | DGZ_GATHER_FLAG_STREAM_STORES | DGZ_GATHER_FLAG_EVICT_FIRST_LOADS |
+                   DGZ_GATHER_FLAG_DYNAMIC)) == 0) {
         flags |= DGZ_GATHER_FLAG_DEEP;
         if (variant == DGZ_GATHER_SEGMENT && !cache) {
             // Translation-bound regime (explore19-22): below ~1 KiB per row
@@ -461,11 +487,17 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
             }
         }
         const int sw = (int)(x & (~x + 1));
-        SegLaunch L{cache ? &ca : nullptr, flags, dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s};
+        unsigned long long* ctr = nullptr;
+        if (flags & DGZ_GATHER_FLAG_DYNAMIC) {
+            DGZ_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), s));
+            DGZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
+        }
+        SegLaunch L{cache ? &ca : nullptr, flags, dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s, ctr};
         if (idx_is64)
             e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, L);
         else
             e = launch_segment_sw<int32_t>(sw, t, (const int32_t*)idx, L);
+        if (ctr) cudaFreeAsync(ctr, s);
     } else if (variant == DGZ_GATHER_NAIVE || variant == DGZ_GATHER_SHIFT) {
         int64_t blocks = (int64_t)k * 4;
         const bool sh = variant == DGZ_GATHER_SHIFT;

@@ -28,7 +28,7 @@ HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM, HOST_CUDA_PINNED, HOST_HUGETLB_2M, HOST_
 HOST_NUMA_INTERLEAVE = 64
 GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
 SCHED_AUTO, SCHED_INTERLEAVED, SCHED_BLOCKED = range(3)
-FLAG_NO_MERGE, FLAG_DEEP, FLAG_ORDER, FLAG_STREAM_STORES, FLAG_EVICT_FIRST_LOADS = 1, 2, 4, 8, 16
+FLAG_NO_MERGE, FLAG_DEEP, FLAG_ORDER, FLAG_STREAM_STORES, FLAG_EVICT_FIRST_LOADS, FLAG_DYNAMIC = 1, 2, 4, 8, 16, 32
 MAX_FANOUT, MAX_LAYERS = 64, 8
 ELEM_BYTES = {F32: 4, F16: 2, BF16: 2, U8: 1}
 TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16, U8: torch.uint8}

@@ -230,7 +230,7 @@ def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds
     results, best = [], None
     for cand in candidates:
         part = dgz.Partition(cand.get("sms", 0), -1, cand.get("flags", 0), groups=cand.get("groups"))
-        cfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=warps_per_cta, flags=dgz.FLAG_DEEP)
+        cfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=warps_per_cta, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
         s = part.fetch_stream
         b0 = bufs[0]
         dgz.gather_perm(table, b0.ids_sorted, b0.ids_sorted_pos, out, n=b0.bounds[-1], n_dev=b0.sizes_dev[L:L + 1],

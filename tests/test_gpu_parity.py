@@ -331,7 +331,7 @@ def test_bulk_ring_wraparound(dev, R, sms, warps, n):
         t.close()
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 3, 8, 16, 26])
+@pytest.mark.parametrize("flags", [0, 1, 2, 3, 8, 16, 26, 32, 34])
 def test_segment_flags(dev, flags):   # 1 = NO_MERGE (a no-op without dst_pos), 2 = DEEP, 8/16 = L2 cache hints
     R, rows = 520, 5000
     t = HostTable(rows, R, seed=flags, base=8, dtype=dgz.F32)
@@ -541,7 +541,7 @@ def test_fetcher_modes_match_oracle(dev, graphs, sampler_sms):
 
 
 @pytest.mark.parametrize("R,base", [(400, 0), (520, 8), (512, 4), (512, 0), (2408, 0), (132, 64), (128, 16), (100, 4)])
-@pytest.mark.parametrize("flags", [0, 1, 2, 24])
+@pytest.mark.parametrize("flags", [0, 1, 2, 24, 32, 34])
 def test_gather_perm_adjacent_rows_merge(dev, R, base, flags):
     """Sorted lists full of table-adjacent rows: the shared 128 B line of two adjacent rows is
     fetched once and stored to both (MERGE), chains of adjacent rows, batch boundaries, and the
