@@ -389,10 +389,8 @@ def run_ours(args, d: Dist):
                    "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
                    "pipeline": fetcher.mode,
                    "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else "pinned host memory, sampled by zero-copy",
-                   "gather": {"variant": "segment", "sm_count": args.gather_sms or sm_count_all,
-                              "schedule": "work counter" if args.dynamic else "static interleave",
-                              "warps_per_cta": args.gather_warps or 2, "lines_in_flight_per_warp": 64,
-                              "order": "address-sorted + inverse permutation"}},
+                   "gather": dict(dgz.gather_plan(table, cap, True, gcfg),
+                                  order="address-sorted + inverse permutation (dgz_gather_perm)")},
         "per_gpu_gbs": round(per_gpu, 3),
         "roofline": {"bound": "pcie", "achieved": round(gather_gbs, 3), "peak": peak, "unit": "GB/s",
                      "frac": round(gather_gbs / peak, 4), "traffic": traffic, "traffic_detail": traffic_detail,

@@ -185,6 +185,11 @@ typedef struct {
 #define DGZ_GATHER_FLAG_DYNAMIC 32       /* SEGMENT: warps take 32-row batches from a work counter (in
                                             ascending order) instead of a static interleave */
 
+/* The launch a gather of n rows would use (sorted != 0: dgz_gather_perm / the fetcher's sorted
+ * path) with `cfg` (NULL = defaults): the resolved variant, SM count, warps per CTA, CTAs per SM,
+ * schedule and flags in *plan, and the grid size in *ctas (optional).  No GPU work. */
+DGZ_API dgz_status dgz_gather_plan(dgz_table t, int64_t n, int32_t sorted, const dgz_gather_cfg* cfg, dgz_gather_cfg* plan,
+                                   int32_t* ctas);
 /* As dgz_gather, with an optional device-resident row count: when n_dev != NULL the kernel
  * gathers min(*n_dev, n) rows (n is the capacity), so a gather can follow the sampler on the
  * same stream without a host round trip.  cfg may be NULL (defaults). */

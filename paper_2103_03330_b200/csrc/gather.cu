@@ -396,27 +396,13 @@ using namespace dgz;
 dgz_status dgz_gather_bulk(const dgz_table_s* t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n,
                            const int64_t* n_dev, void* out, int* err, int sms, int warps, int blocked, cudaStream_t s);
 
-dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n, const int64_t* n_dev,
-                           void* out, const dgz_gather_cfg* cfg, cudaStream_t s, const dgz_cache_view* cache) {
-    DGZ_REQUIRE(t, "dgz_gather: null table");
-    DGZ_REQUIRE(n >= 0, "dgz_gather: n < 0");
-    if (n == 0) return DGZ_OK;
-    DGZ_REQUIRE(idx && out, "dgz_gather: null idx or out");
-    DGZ_REQUIRE(((uintptr_t)out % (uintptr_t)t->elem_bytes) == 0, "dgz_gather: out not aligned to the element size");
-    {
-        const uint8_t* o = (const uint8_t*)out;
-        const uint8_t* tb = t->host;
-        const uint8_t* te = t->host + t->rows * t->row_bytes;
-        DGZ_REQUIRE(o + n * t->row_bytes <= tb || o >= te, "dgz_gather: out aliases the table");
-    }
-    int dev = 0;
-    DGZ_CUDA(cudaGetDevice(&dev));
-    if (dev != t->device && !(t->flags & (DGZ_REG_PORTABLE | DGZ_REG_VMM_BACKED))) {
-        set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
-        return DGZ_ERR_STATE;
-    }
-    int* err = dgz_table_flag(t);
-    if (!err) { set_error("dgz_gather: cannot allocate the device flag"); return DGZ_ERR_CUDA; }
+// Launch shape of a gather: the caller's cfg where given, else the measured defaults (DESIGN.md
+// section 5).  Shared by the gathers and dgz_gather_plan (which reports it).
+struct LaunchPlan {
+    int variant, k, warps, cps, flags, blocked;
+};
+
+static LaunchPlan plan_launch(const dgz_table_s* t, int64_t n, bool sorted_path, const dgz_gather_cfg* cfg, bool cache) {
     const int nsm = sm_count_of_current_device();
     int variant = cfg ? cfg->variant : DGZ_GATHER_AUTO;
     if (variant == DGZ_GATHER_AUTO) variant = DGZ_GATHER_SEGMENT;
@@ -426,7 +412,6 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     // (dgz_gather_perm): a narrow in-flight window (1-2 warps per SM, 16 line loads per lane,
     // shaped by row width and sparsity below) keeps translations local and still covers the PCIe
     // bandwidth-delay product; it also leaves SMs free.
-    const bool sorted_path = dst_pos != nullptr;
     int k = bounded ? (cfg->sm_count < nsm ? cfg->sm_count : nsm) : nsm;
     const bool hbm_table = t->flags & DGZ_REG_DEVICE;   // HBM-resident: latency-bound, wants many warps
     int warps = (cfg && cfg->warps_per_cta > 0) ? cfg->warps_per_cta
@@ -463,6 +448,32 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     if (warps * cps > 64) cps = 64 / warps > 0 ? 64 / warps : 1;
     const int sched = cfg ? cfg->schedule : DGZ_SCHED_AUTO;
     const int blocked = sched == DGZ_SCHED_BLOCKED;
+    return LaunchPlan{variant, k, warps, cps, flags, blocked};
+}
+
+dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n, const int64_t* n_dev,
+                           void* out, const dgz_gather_cfg* cfg, cudaStream_t s, const dgz_cache_view* cache) {
+    DGZ_REQUIRE(t, "dgz_gather: null table");
+    DGZ_REQUIRE(n >= 0, "dgz_gather: n < 0");
+    if (n == 0) return DGZ_OK;
+    DGZ_REQUIRE(idx && out, "dgz_gather: null idx or out");
+    DGZ_REQUIRE(((uintptr_t)out % (uintptr_t)t->elem_bytes) == 0, "dgz_gather: out not aligned to the element size");
+    {
+        const uint8_t* o = (const uint8_t*)out;
+        const uint8_t* tb = t->host;
+        const uint8_t* te = t->host + t->rows * t->row_bytes;
+        DGZ_REQUIRE(o + n * t->row_bytes <= tb || o >= te, "dgz_gather: out aliases the table");
+    }
+    int dev = 0;
+    DGZ_CUDA(cudaGetDevice(&dev));
+    if (dev != t->device && !(t->flags & (DGZ_REG_PORTABLE | DGZ_REG_VMM_BACKED))) {
+        set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
+        return DGZ_ERR_STATE;
+    }
+    int* err = dgz_table_flag(t);
+    if (!err) { set_error("dgz_gather: cannot allocate the device flag"); return DGZ_ERR_CUDA; }
+    const LaunchPlan P = plan_launch(t, n, dst_pos != nullptr, cfg, cache != nullptr);
+    const int variant = P.variant, k = P.k, warps = P.warps, cps = P.cps, flags = P.flags, blocked = P.blocked;
     DGZ_REQUIRE(!dst_pos || variant == DGZ_GATHER_SEGMENT || variant == DGZ_GATHER_BULK,
                 "dgz_gather: destination permutation needs the SEGMENT or BULK variant");
 
@@ -582,4 +593,25 @@ extern "C" dgz_status dgz_gather_cached(dgz_table t, const dgz_cache_view* cache
     DGZ_REQUIRE(!cfg || cfg->variant == DGZ_GATHER_AUTO || cfg->variant == DGZ_GATHER_SEGMENT,
                 "dgz_gather_cached: only the SEGMENT variant reads the cache");
     return dgz_gather_impl(t, idx_dev, 1, dst_pos_dev, n, n_dev, out_dev, cfg, (cudaStream_t)stream, cache);
+}
+
+extern "C" dgz_status dgz_gather_plan(dgz_table t, int64_t n, int32_t sorted, const dgz_gather_cfg* cfg, dgz_gather_cfg* plan,
+                                      int32_t* ctas) {
+    DGZ_REQUIRE(t && plan && n > 0, "dgz_gather_plan: null table/plan or n <= 0");
+    const LaunchPlan P = plan_launch(t, n, sorted != 0, cfg, false);
+    plan->variant = P.variant;
+    plan->sm_count = P.k;
+    plan->warps_per_cta = P.warps;
+    plan->ctas_per_sm = P.cps;
+    plan->schedule = P.blocked ? DGZ_SCHED_BLOCKED : DGZ_SCHED_INTERLEAVED;
+    plan->flags = P.flags;
+    if (ctas) {
+        int64_t blocks = (int64_t)P.k * P.cps;
+        if (P.variant == DGZ_GATHER_SEGMENT) {
+            const int64_t need = ((n + 31) / 32 + P.warps - 1) / P.warps;
+            if (blocks > need) blocks = need;
+        }
+        *ctas = (int32_t)blocks;
+    }
+    return DGZ_OK;
 }

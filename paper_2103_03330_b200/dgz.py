@@ -120,6 +120,7 @@ _SIGS = {
     "dgz_gather_i32": ([_vp, _vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_gather_ex": ([_vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
     "dgz_gather_perm": ([_vp, _vp, _vp, _i64, _vp, _vp, _P(GatherCfg), _vp], ctypes.c_int),
+    "dgz_gather_plan": ([_vp, _i64, _i32, _P(GatherCfg), _P(GatherCfg), _P(_i32)], ctypes.c_int),
     "dgz_order_workspace_bytes": ([_i64, _P(_sz)], ctypes.c_int),
     "dgz_order_ids": ([_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp], ctypes.c_int),
     "dgz_check_errors": ([_vp, _vp], ctypes.c_int),
@@ -382,6 +383,23 @@ def unregister_table(t: Table) -> None:
 def gather_cfg(variant: int = GATHER_AUTO, sm_count: int = 0, warps_per_cta: int = 0, ctas_per_sm: int = 0,
                schedule: int = SCHED_AUTO, flags: int = 0) -> GatherCfg:
     return GatherCfg(variant, sm_count, warps_per_cta, ctas_per_sm, schedule, flags)
+
+
+VARIANT_NAMES = {GATHER_SEGMENT: "segment", GATHER_NAIVE: "naive", GATHER_SHIFT: "shift", GATHER_BULK: "bulk"}
+
+
+def gather_plan(table: Table, n: int, sorted_ids: bool = True, cfg: GatherCfg | None = None) -> dict:
+    """The launch a gather of n rows would use (dgz_gather_plan): variant, SMs, warps per CTA, CTAs,
+    line loads in flight per lane, schedule, flags."""
+    plan, ctas = GatherCfg(), _i32()
+    _check(_lib.dgz_gather_plan(table.handle, int(n), int(bool(sorted_ids)), ctypes.byref(cfg) if cfg is not None else None,
+                                ctypes.byref(plan), ctypes.byref(ctas)), "dgz_gather_plan")
+    return {"variant": VARIANT_NAMES.get(plan.variant, plan.variant), "sm_count": plan.sm_count,
+            "warps_per_cta": plan.warps_per_cta, "ctas": ctas.value,
+            "line_loads_per_lane": 16 if plan.flags & FLAG_DEEP else 8,
+            "schedule": ("work counter" if plan.flags & FLAG_DYNAMIC else
+                         ("blocked" if plan.schedule == SCHED_BLOCKED else "static interleave")),
+            "flags": plan.flags}
 
 
 def gather(table: Table, idx: torch.Tensor, out: torch.Tensor, n: int | None = None, n_dev: torch.Tensor | None = None,

@@ -574,17 +574,22 @@ def test_gather_perm_adjacent_rows_merge(dev, R, base, flags):
         t.close()
 
 
-@pytest.mark.parametrize("R,rows,n", [(128, 4_000_000, 3000),     # > 150 KiB apart: half the SMs, 1 warp
-                                      (128, 400_000, 60_000),      # dense small rows: every SM, 1 warp
-                                      (400, 2_000_000, 5000),      # 4 lines, sparse: 1 warp per SM
-                                      (400, 200_000, 80_000),      # 4 lines, dense: 2 warps per SM
-                                      (1028, 600_000, 2000),       # >= 8 lines: 2 warps per SM
-                                      (64, 8_000_000, 1000)])
-def test_gather_perm_default_launch_shapes(dev, R, rows, n):
-    """Every branch of the sorted gather's default launch-shape rule (row width x sparsity) moves the
-    same bytes as the oracle."""
+@pytest.mark.parametrize("R,rows,n,shape", [(128, 4_000_000, 3000, ("half", 1)),     # > 150 KiB apart
+                                            (128, 400_000, 60_000, ("all", 1)),      # dense small rows
+                                            (400, 2_000_000, 5000, ("half", 1)),     # 4 lines, > 150 KiB apart
+                                            (400, 2_000_000, 8000, ("all", 1)),      # 4 lines, 100 KiB apart
+                                            (400, 200_000, 80_000, ("all", 2)),      # 4 lines, dense
+                                            (1028, 600_000, 2000, ("all", 2)),       # >= 8 lines
+                                            (64, 8_000_000, 1000, ("half", 1))])
+def test_gather_perm_default_launch_shapes(dev, R, rows, n, shape):
+    """Every branch of the sorted gather's default launch-shape rule (row width x sparsity): the
+    plan dgz_gather_plan reports, and the same bytes as the oracle."""
     t = HostTable(rows, R, seed=R + n, base=4, dtype=dgz.F32)
     try:
+        plan = dgz.gather_plan(t.table, n, True)
+        nsm = dgz.device_sm_count()
+        assert (plan["sm_count"], plan["warps_per_cta"]) == ((nsm if shape[0] == "all" else nsm // 2), shape[1]), plan
+        assert plan["line_loads_per_lane"] == 16 and plan["variant"] == "segment"
         idx = gen.random_ids(rows, n, seed=n)
         want, _ = oracle.gather(t.np, R, idx)
         srt, pos = dgz.order_ids(torch.from_numpy(idx).cuda(), rows)
