@@ -264,7 +264,7 @@ def hbm_peak() -> float:
 
 def load_profile_traffic(cid):
     """(dram bytes per gather launch, summary) from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_gather_summary.json")
+    p = os.path.join(ROOT, "profiles", "r01", "ncu_gather_summary.json")
     try:
         with open(p) as f:
             c = json.load(f).get(f"config{cid}")

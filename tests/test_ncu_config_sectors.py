@@ -1,4 +1,4 @@
-"""The committed ncu captures of one bench gather per config (profiles/ncu_gather_summary.json:
+"""The committed ncu captures of one bench gather per config (profiles/r01/ncu_gather_summary.json:
 launch 4 of `bench.py --config c --steps 3 --warmup 3`, i.e. global batch j = 3) read exactly the
 sectors the oracle's request model predicts for that minibatch: the distinct 32 B sectors of each
 32-row batch of the address-sorted U (merged plan), U drawn by the oracle sampler.  CPU only."""
@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.parametrize("cid", [2, 3, 4])
 def test_ncu_sysmem_sectors_match_request_model(cid):
-    with open(os.path.join(ROOT, "profiles", "ncu_gather_summary.json")) as f:
+    with open(os.path.join(ROOT, "profiles", "r01", "ncu_gather_summary.json")) as f:
         cap = json.load(f)[f"config{cid}"]
     src = cap["source"]     # config 4 is bench.py's default (no --config flag in its command)
     assert (f"--config {cid}" in src or f"(config {cid}," in src) and "--warmup 3" in src and "launch 4" in src

@@ -1,4 +1,4 @@
-"""Summarise an `ncu --set full` capture of the gather into profiles/ncu_gather_summary.json."""
+"""Summarise an `ncu --set full` capture of the gather into profiles/r01/ncu_gather_summary.json."""
 import csv
 import io
 import json
