@@ -208,12 +208,14 @@ def measure_ceilings(dgz, d: Dist):
     rank's; the aggregate = sum of bytes / max time over ranks is the host/root-complex limit
     the N-GPU value is compared with): H2D DMA from pinned memory, zero-copy streaming read."""
     h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    h[::4096] = 1                                   # touch every page of the staging buffer
     dbuf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for _ in range(3):
+    for _ in range(40):                             # warm-up: the first ~50 copies ramp from ~43 to ~55 GB/s
         dbuf.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
     a, b = ev(), ev()
     trials, agg = [], []
-    for _ in range(5):  # best of 5 x (10 copies of 256 MiB), all ranks concurrently
+    for _ in range(8):  # best of 8 x (10 copies of 256 MiB), all ranks concurrently
         torch.cuda.synchronize()
         d.barrier()
         a.record()
@@ -248,7 +250,8 @@ def measure_ceilings(dgz, d: Dist):
     del dbuf
     return {"h2d_dma_gbs": round(dma, 2), "h2d_dma_trials": [round(x, 2) for x in trials], "zc_stream_gbs": round(zc, 2),
             "ranks": d.world, "h2d_dma_aggregate_gbs": round(max(agg), 2), "zc_stream_aggregate_gbs": round(zc_agg, 2),
-            "how": "every rank at once after a barrier: best of 5 x (cudaMemcpyAsync 256 MiB pinned H2D x10); zero-copy "
+            "how": "every rank at once after a barrier: best of 8 x (cudaMemcpyAsync 256 MiB pinned H2D x10) after 40 "
+                   "warm-up copies; zero-copy "
                    "LDG.128 stream over a 1 GiB pinned buffer x4 on 8 SMs; aggregate = sum bytes / max time over ranks"}
 
 
