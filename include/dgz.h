@@ -2,7 +2,7 @@
  * dgz.h -- C ABI of libdgz: direct GPU zero-copy feature gather for GCN minibatches on B200.
  *
  * The operations follow arXiv 2103.03330 (PyTorch-Direct); "P:n" is /root/reference/PAPER.md
- * line n, "S:n" is SPEC.md line n.  The boundary is described in DESIGN.md section 2.
+ * line n, "S:n" is SPEC.md line n.  The boundary is described in DESIGN.md section 1.
  *
  * Conventions for every entry point
  *   - Returns a dgz_status.  No exception crosses the ABI and nothing calls exit().
@@ -74,9 +74,11 @@ DGZ_API uint64_t dgz_kernel_launches(void);
                                         touch (a no-op on one node): multi-socket boxes whose G GPUs all
                                         read the one shared table (SURVEY 7 "host aggregate") */
 #define DGZ_HOST_VMM 4u      /* CUDA VMM host allocation (cuMemCreate on host NUMA node 0): pinned,
-                                CPU-accessible, mapped into the current GPU with large pages at the
-                                same address.  Needs a CUDA device; shm_name must be NULL (share it
-                                across processes with dgz_host_export / dgz_host_import). */
+                                CPU-accessible, mapped into the current GPU at the same address (with
+                                2 MiB allocation granularity; the GPU still translated it at 4 KiB pages
+                                on the measured boxes).  Needs a CUDA device;
+                                shm_name must be NULL (share it across processes with dgz_host_export /
+                                dgz_host_import). */
 
 /* Number of online NUMA nodes of the host (1 when unknown). */
 DGZ_API int dgz_host_numa_nodes(void);
@@ -106,7 +108,7 @@ DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 #define DGZ_REG_NO_PIN 4u    /* memory is already page-locked (e.g. cudaHostAlloc): map only */
 #define DGZ_REG_DEVICE 16u    /* (reported) a device-resident table wrapped by dgz_wrap_device_table */
 #define DGZ_REG_VMM_BACKED 8u /* (reported in dgz_table_info.flags) the table lies in a DGZ_HOST_VMM
-                                 allocation: no cudaHostRegister, large-page GPU mapping */
+                                 allocation: no cudaHostRegister, mapped by the VMM allocation itself */
 
 /* host_ptr: row 0 of a row-major, unpadded rows x dim table of `dtype` elements in host
  * memory (any alignment; unaligned bases are a first-class case, S:37 base_offset).  The caller
@@ -183,7 +185,8 @@ typedef struct {
 #define DGZ_GATHER_FLAG_STREAM_STORES 8  /* SEGMENT: HBM stores as st.global.cs (evict-first in L2) */
 #define DGZ_GATHER_FLAG_EVICT_FIRST_LOADS 16 /* SEGMENT: zero-copy loads under an L2 evict_first policy */
 #define DGZ_GATHER_FLAG_DYNAMIC 32       /* SEGMENT: warps take 32-row batches from a work counter (in
-                                            ascending order) instead of a static interleave */
+                                            ascending order) instead of a static interleave; the 8-byte
+                                            counter comes from the stream-ordered pool (cudaMallocAsync) */
 
 /* The launch a gather of n rows would use (sorted != 0: dgz_gather_perm / the fetcher's sorted
  * path) with `cfg` (NULL = defaults): the resolved variant, SM count, warps per CTA, CTAs per SM,
