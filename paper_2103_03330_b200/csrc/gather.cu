@@ -440,6 +440,12 @@ static LaunchPlan plan_launch(const dgz_table_s* t, int64_t n, bool sorted_path,
                 k = nsm;
                 warps = 1;
             }
+        } else if (variant == DGZ_GATHER_SEGMENT && cache) {
+            // cached gather: the rows left for PCIe are the sparse part of the list (the hot rows
+            // come from HBM), i.e. the translation-bound regime -- one warp per SM (explore30:
+            // 5 % / 20 % cached on the power-law graph, 54 -> 67 / 78 -> 91 GB/s effective)
+            k = nsm;
+            warps = 1;
         }
     }
     const int max_warps = variant == DGZ_GATHER_SEGMENT ? 16 : 32;  // SEGMENT: <= 512 threads (128 regs)
