@@ -6,7 +6,7 @@ width over the 56.9 GB buffer (base offset 0 and 4), useful GB/s (GB = 1e9).
   dma : torch.index_select with all host threads into pinned staging, 32 MiB chunks, each chunk's
         cudaMemcpyAsync H2D overlapping the CPU gather of the next (double-buffered)
 
-    python tools/sweep_dma_vs_zc.py [--zc-only] [--widths=66,202,...] > gpurun_out/sweep_dma_vs_zc.jsonl
+    python tools/sweep_dma_vs_zc.py [--zc-only] [--widths=66,202,...] [--threads=T] > gpurun_out/sweep_dma_vs_zc.jsonl
 """
 import json
 import os
@@ -21,6 +21,9 @@ from paper_2103_03330_b200 import dgz  # noqa: E402
 
 torch.cuda.set_device(0)
 threads = os.cpu_count() or 1
+for a in sys.argv[1:]:
+    if a.startswith("--threads="):         # e.g. the host-core share of one GPU on an 8-GPU box
+        threads = int(a.split("=", 1)[1])
 torch.set_num_threads(threads)
 total = gen.CONFIGS[4].table_bytes
 buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_HUGEPAGE)
