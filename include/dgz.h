@@ -70,9 +70,10 @@ DGZ_API uint64_t dgz_kernel_launches(void);
                                    (single process; not shareable by name) */
 #define DGZ_HOST_HUGETLB_2M 16u /* anonymous MAP_HUGETLB 2 MiB pages (needs vm.nr_hugepages) */
 #define DGZ_HOST_HUGETLB_1G 32u /* anonymous MAP_HUGETLB 1 GiB pages */
-#define DGZ_HOST_NUMA_INTERLEAVE 64u /* mbind(MPOL_INTERLEAVE) over the online NUMA nodes before first
+#define DGZ_HOST_NUMA_INTERLEAVE 64u /* mbind(MPOL_INTERLEAVE) over the allowed NUMA nodes before first
                                         touch (a no-op on one node): multi-socket boxes whose G GPUs all
-                                        read the one shared table (SURVEY 7 "host aggregate") */
+                                        read the one shared table (SURVEY 7 "host aggregate"); a hint:
+                                        if the kernel refuses it the mapping keeps first-touch placement */
 #define DGZ_HOST_VMM 4u      /* CUDA VMM host allocation (cuMemCreate on host NUMA node 0): pinned,
                                 CPU-accessible, mapped into the current GPU at the same address (with
                                 2 MiB allocation granularity; the GPU still translated it at 4 KiB pages
@@ -80,7 +81,7 @@ DGZ_API uint64_t dgz_kernel_launches(void);
                                 shm_name must be NULL (share it across processes with dgz_host_export /
                                 dgz_host_import). */
 
-/* Number of online NUMA nodes of the host (1 when unknown). */
+/* Number of NUMA nodes this process may allocate on (cpuset Mems_allowed; 1 when unknown). */
 DGZ_API int dgz_host_numa_nodes(void);
 /* Map `bytes` of host memory.  shm_name == NULL: private anonymous mapping.  Otherwise a POSIX
  * shared-memory object (/dev/shm/<name>): create != 0 creates/truncates it to `bytes`,

@@ -74,13 +74,31 @@ extern "C" uint64_t dgz_kernel_launches(void) { return g_launches.load(); }
 // ---------------------------------------------------------------------------------------------
 // Host table manager
 // ---------------------------------------------------------------------------------------------
-// Online NUMA nodes (/sys/devices/system/node/online, e.g. "0-1" or "0,2-3") as a bit mask.
+// NUMA nodes this process may allocate on, as a bit mask: the cpuset's Mems_allowed_list from
+// /proc/self/status (a container may restrict it), else /sys/devices/system/node/online; lists
+// look like "0-1" or "0,2-3".
 static int numa_online_mask(unsigned long* mask, int max_nodes) {
-    FILE* f = fopen("/sys/devices/system/node/online", "r");
-    if (!f) return 1;   // no NUMA information: treat as one node
-    char line[256] = {0};
-    if (!fgets(line, sizeof line, f)) line[0] = 0;
-    fclose(f);
+    char line[512] = {0};
+    bool found = false;
+    if (FILE* st = fopen("/proc/self/status", "r")) {
+        char buf[512];
+        while (fgets(buf, sizeof buf, st)) {
+            if (strncmp(buf, "Mems_allowed_list:", 18) == 0) {
+                const char* v = buf + 18;
+                while (*v == ' ' || *v == '\t') ++v;
+                strncpy(line, v, sizeof line - 1);
+                found = true;
+                break;
+            }
+        }
+        fclose(st);
+    }
+    if (!found) {
+        FILE* f = fopen("/sys/devices/system/node/online", "r");
+        if (!f) return 1;   // no NUMA information: treat as one node
+        if (!fgets(line, sizeof line, f)) line[0] = 0;
+        fclose(f);
+    }
     int count = 0;
     for (char* tok = strtok(line, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
         int lo = 0, hi = 0;
@@ -157,11 +175,10 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
         unsigned long mask[max_nodes / (8 * sizeof(unsigned long))] = {0};
         if (numa_online_mask(mask, max_nodes) > 1) {
             const int mpol_interleave = 3;   // MPOL_INTERLEAVE (linux/mempolicy.h)
-            if (syscall(SYS_mbind, p, bytes, mpol_interleave, mask, (unsigned long)max_nodes, 0u) != 0) {
-                set_error("mbind(MPOL_INTERLEAVE, %zu bytes): %s", bytes, strerror(errno));
-                munmap(p, bytes);
-                return DGZ_ERR_INVALID;
-            }
+            // a placement hint, not a requirement: if the kernel refuses it the mapping keeps the
+            // default first-touch policy (and dgz_last_error says why)
+            if (syscall(SYS_mbind, p, bytes, mpol_interleave, mask, (unsigned long)max_nodes, 0u) != 0)
+                set_error("mbind(MPOL_INTERLEAVE, %zu bytes) ignored: %s", bytes, strerror(errno));
         }
     }
     if (flags & DGZ_HOST_HUGEPAGE) madvise(p, bytes, MADV_HUGEPAGE);
