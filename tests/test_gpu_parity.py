@@ -630,3 +630,35 @@ def test_tune_fetch_partition_then_fetch(dev):
         part.destroy()
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("R,base", [(8 << 20, 0), ((8 << 20) + 36, 4), ((32 << 20) - 4, 8)])
+def test_gather_very_large_rows(dev, R, base):
+    """Rows up to the SEGMENT limit (< 32 MiB per row): every line of every row, unsorted and
+    sorted, at aligned and misaligned bases; 32 MiB rows are refused synchronously."""
+    rows = 6
+    t = HostTable(rows, R, seed=R % 1000, base=base, dtype=dgz.F32)
+    try:
+        idx = np.array([3, 0, 5, 3], dtype=np.int64)
+        want, _ = oracle.gather(t.np, R, idx)
+        assert np.array_equal(_gather_dev(t, idx), want)
+        order = np.argsort(idx, kind="stable")
+        out = torch.full((idx.shape[0] * R,), 0xAB, dtype=torch.uint8, device="cuda")
+        dgz.gather_perm(t.table, torch.from_numpy(idx[order]).cuda(), torch.from_numpy(order.astype(np.int64)).cuda(), out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+    finally:
+        t.close()
+
+
+def test_gather_refuses_rows_of_32_mib(dev):
+    R = 32 << 20
+    buf = dgz.HostBuffer(R + 4096)
+    t = dgz.register_table(buf.ptr, 1, R // 4, dgz.F32)
+    try:
+        out = torch.empty(R, dtype=torch.uint8, device="cuda")
+        with pytest.raises(dgz.DgzError):
+            dgz.gather(t, torch.zeros(1, dtype=torch.int64, device="cuda"), out)
+    finally:
+        t.unregister()
+        buf.free()
