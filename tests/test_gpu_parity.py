@@ -662,3 +662,13 @@ def test_gather_refuses_rows_of_32_mib(dev):
     finally:
         t.unregister()
         buf.free()
+
+
+def test_sampler_limits(dev):
+    """DGZ_MAX_LAYERS hops, DGZ_MAX_FANOUT on high-degree nodes (Floyd with f = 64), and every node
+    of the graph as a seed (U = all nodes)."""
+    off, col = gen.gen_csr(30_000, 100.0, 77)
+    _compare_plan(off, col, gen.batch_seeds(30_000, 64, 77, 0), (dgz.MAX_FANOUT,), 5)
+    _compare_plan(off, col, gen.batch_seeds(30_000, 16, 77, 1), (2,) * dgz.MAX_LAYERS, 6)
+    off, col = gen.gen_csr(5000, 6.0, 78)
+    _compare_plan(off, col, np.arange(5000, dtype=np.int64)[::-1].copy(), (3, 2), 7)
