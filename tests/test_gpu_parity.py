@@ -672,3 +672,37 @@ def test_sampler_limits(dev):
     _compare_plan(off, col, gen.batch_seeds(30_000, 16, 77, 1), (2,) * dgz.MAX_LAYERS, 6)
     off, col = gen.gen_csr(5000, 6.0, 78)
     _compare_plan(off, col, np.arange(5000, dtype=np.int64)[::-1].copy(), (3, 2), 7)
+
+
+def test_concurrent_streams(dev):
+    """Two samplers and two gathers (one with the work-counter schedule) in flight at once on two
+    streams over the same graph and table: both minibatches equal the oracle's."""
+    c = gen.CONFIGS[1]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        bufs = [dgz.SampleBuffers(c.n_nodes, c.batch, c.fanouts) for _ in range(2)]
+        outs = [torch.empty(bufs[0].bounds[-1] * c.row_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        L = len(c.fanouts)
+        js = (2, 7)
+        for k in range(2):
+            s = streams[k]
+            seeds = torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, js[k])).to("cuda", non_blocking=True)
+            s.wait_stream(torch.cuda.current_stream())
+            dgz.sample_uniform(g, seeds, c.fanouts, gen.batch_rng_seed(c.seed, js[k]), bufs[k], stream=s)
+            b = bufs[k]
+            dgz.gather_perm(t.table, b.ids_sorted, b.ids_sorted_pos, outs[k], n=b.bounds[-1], n_dev=b.sizes_dev[L:L + 1],
+                            cfg=dgz.gather_cfg(flags=dgz.FLAG_DYNAMIC if k else 0), stream=s)
+        torch.cuda.synchronize()
+        for k in range(2):
+            seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, js[k])
+            want = oracle.sample_uniform(off, col, seeds, c.fanouts, gen.batch_rng_seed(c.seed, js[k]), with_blocks=False)
+            n = want.U.shape[0]
+            exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+            assert np.array_equal(bufs[k].ids[:n].cpu().numpy(), want.U)
+            assert np.array_equal(outs[k][:n * c.row_bytes].cpu().numpy().reshape(n, -1), exp)
+        dgz.check_errors(t.table)
+    finally:
+        t.close()
