@@ -60,6 +60,8 @@ class MinibatchFetcher:
                  gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None,
                  overlap_sampling: bool = False, sample_stream=None, sampler_sms: int | None = None, graphs: bool = False):
         self.table, self.graph = table, graph
+        # an HBM-resident table (dgz.DeviceTable) is gathered in frontier order (explore31)
+        self.hbm_table = bool(table.info.flags & dgz.REG_DEVICE)
         if sampler_sms is None:
             # A zero-copy CSR (dgz.HostGraph) makes the sampler a stream of small PCIe reads: beside
             # the gather both slow down (36 vs 37.8 GB/s sequential, config 4), so it runs back to
@@ -150,8 +152,12 @@ class MinibatchFetcher:
         with torch.cuda.stream(gs):
             if ev:
                 ev[1].record(gs)
-            dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
-                            n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=gs)
+            if self.hbm_table:   # All-in-GPU: no address translation to save; write rows in order
+                dgz.gather(self.table, b.ids, self.rows[p], n=b.bounds[-1], n_dev=b.sizes_dev[L:L + 1],
+                           cfg=self.cfg or dgz.gather_cfg(), stream=gs)
+            else:
+                dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
+                                n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=gs)
             if ev:
                 ev[2].record(gs)
             if count_into is not None:
@@ -164,8 +170,12 @@ class MinibatchFetcher:
         b = self.bufs[p]
         L = len(self.fanouts)
         dgz.sample_uniform(self.graph, self.seed_stage[p], self.fanouts, 0, b, stream=self.stream)
-        dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
-                        n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=self.stream)
+        if self.hbm_table:
+            dgz.gather(self.table, b.ids, self.rows[p], n=b.bounds[-1], n_dev=b.sizes_dev[L:L + 1],
+                       cfg=self.cfg or dgz.gather_cfg(), stream=self.stream)
+        else:
+            dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
+                            n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=self.stream)
 
     def _fetch_graph(self, p, seeds, rng_seed, ev, count_into):
         """Sampler + gather of slot p as one CUDA-graph replay: seeds and the sampler seed are
