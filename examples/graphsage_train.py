@@ -238,6 +238,7 @@ def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--dim", type=int, default=0, help="override the feature dimension (fig:eval_sweep analogue)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--hidden", type=int, default=256)
     ap.add_argument("--classes", type=int, default=172)      # ogbn-papers100M has 172 classes
@@ -260,6 +261,9 @@ def main():
         dist.init_process_group("gloo" if same else "nccl")
     torch.backends.cuda.matmul.allow_tf32 = True
     c = gen.CONFIGS[a.config]
+    if a.dim:
+        import dataclasses
+        c = dataclasses.replace(c, dim=a.dim)
     K = a.steps
     if G == 1:
         buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_HUGEPAGE)
@@ -282,7 +286,7 @@ def main():
     batches = [i * G + rank for i in range(K + 2)]          # seed partition: global batch j = i*G + rank
     seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in batches]
     rng = [gen.batch_rng_seed(c.seed, j) for j in batches]
-    res = {"config": c.name, "steps": K, "ranks": G, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
+    res = {"config": c.name, "dim": c.dim, "steps": K, "ranks": G, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
                                                               f"{a.classes} classes, Adam, fp32 (TF32 matmuls)"
                                                               + (", DDP" if G > 1 else "")}
     modes = a.modes.split(",")
