@@ -374,6 +374,10 @@ DGZ_API dgz_status dgz_partition_destroy(dgz_partition p);
 /* Streaming zero-copy read of `bytes` (multiple of 16) from a mapped host pointer with 16 B
  * loads, `warps` warps on each of `sm_count` SMs, each warp keeping `unroll` loads in flight.
  * A checksum is written to *sink_dev so the loads cannot be elided. */
+/* As dgz_probe_stream (unroll 8) with the loads' L2 prefetch-size hint set to l2_prefetch_bytes
+ * (0 = none, 64, 128, 256): whether GPU-initiated sysmem reads can be made larger than a line. */
+DGZ_API dgz_status dgz_probe_stream_hint(const void* src_dev, int64_t bytes, int32_t sm_count, int32_t warps,
+                                         int32_t l2_prefetch_bytes, uint64_t* sink_dev, dgz_stream stream);
 DGZ_API dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32_t sm_count, int32_t warps,
                             int32_t unroll, uint64_t* sink_dev, dgz_stream stream);
 /* Dependent-load chain of `steps` hops through a mapped host array of int64 "next" offsets;

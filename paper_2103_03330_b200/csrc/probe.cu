@@ -11,7 +11,26 @@ __device__ __forceinline__ uint4 ld_zc(uint64_t p) {
     return r;
 }
 
-template <int U>
+// the same load with an L2 prefetch-size hint (PTX .L2::64B / ::128B / ::256B): does the L2 then
+// fetch 256 B from system memory per miss (fewer, larger PCIe reads)?
+template <int PF>
+__device__ __forceinline__ uint4 ld_zc_pf(uint64_t p) {
+    uint4 r;
+    if constexpr (PF == 256)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if constexpr (PF == 128)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if constexpr (PF == 64)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else
+        r = ld_zc(p);
+    return r;
+}
+
+template <int U, int PF = 0>
 __global__ void __launch_bounds__(1024, 1) stream_kernel(const uint8_t* __restrict__ src, int64_t chunks, uint64_t* sink) {
     const int lane = threadIdx.x & 31;
     const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -22,7 +41,7 @@ __global__ void __launch_bounds__(1024, 1) stream_kernel(const uint8_t* __restri
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t c = c0 + u * 32 + lane;
-            if (c < chunks) v[u] = ld_zc((uint64_t)src + (uint64_t)c * 16);
+            if (c < chunks) v[u] = ld_zc_pf<PF>((uint64_t)src + (uint64_t)c * 16);
             else v[u] = make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
@@ -81,6 +100,25 @@ extern "C" dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32
         default: stream_kernel<8><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); dgz::count_launch(); break;
     }
     return launch_check("stream_kernel");
+}
+
+extern "C" dgz_status dgz_probe_stream_hint(const void* src_dev, int64_t bytes, int32_t sm_count, int32_t warps,
+                                            int32_t l2_prefetch_bytes, uint64_t* sink_dev, dgz_stream stream) {
+    DGZ_REQUIRE(src_dev && sink_dev && bytes > 0 && bytes % 16 == 0 && ((uintptr_t)src_dev % 16) == 0,
+                "dgz_probe_stream_hint: bad args");
+    const int nsm = sm_count_of_current_device();
+    const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
+    if (warps <= 0 || warps > 32) warps = 32;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t chunks = bytes / 16;
+    switch (l2_prefetch_bytes) {
+        case 64: stream_kernel<8, 64><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        case 128: stream_kernel<8, 128><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        case 256: stream_kernel<8, 256><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+        default: stream_kernel<8, 0><<<k, warps * 32, 0, s>>>((const uint8_t*)src_dev, chunks, sink_dev); break;
+    }
+    dgz::count_launch();
+    return launch_check("stream_kernel (hint)");
 }
 
 extern "C" dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream) {

@@ -136,6 +136,7 @@ _SIGS = {
     "dgz_partition_destroy": ([_vp], ctypes.c_int),
     "dgz_probe_stream": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
+    "dgz_probe_stream_hint": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_spin": ([_i32, _i32, _i64, _vp, _vp], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -645,6 +646,12 @@ def aggregate_mean(x: torch.Tensor, dim: int, nbr_local: torch.Tensor, cnt: torc
 def probe_stream(src_dev_ptr: int, nbytes: int, sm_count: int, warps: int, unroll: int, sink: torch.Tensor, stream=None):
     _check(_lib.dgz_probe_stream(src_dev_ptr, nbytes, sm_count, warps, unroll, _dptr(sink), _stream(stream)),
            "dgz_probe_stream")
+
+
+def probe_stream_hint(src_dev_ptr: int, nbytes: int, sm_count: int, warps: int, l2_prefetch_bytes: int, sink: torch.Tensor,
+                      stream=None):
+    _check(_lib.dgz_probe_stream_hint(src_dev_ptr, nbytes, sm_count, warps, l2_prefetch_bytes, _dptr(sink), _stream(stream)),
+           "dgz_probe_stream_hint")
 
 
 def probe_chase(src_dev_ptr: int, steps: int, cycles: torch.Tensor, stream=None):
