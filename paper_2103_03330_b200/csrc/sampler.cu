@@ -291,6 +291,8 @@ constexpr int kSmallSeeds = 4096;  // 32 KiB of dynamic shared memory: no opt-in
 __global__ void __launch_bounds__(1024)
 seeds_small_kernel(const int64_t* __restrict__ seeds, int n, int64_t N, int64_t* __restrict__ U, uint32_t* __restrict__ front,
                    int32_t* __restrict__ pos, int64_t* __restrict__ sizes, int* __restrict__ err) {
+    // one block, O(n): the first occurrence of each seed wins an atomicMin on its entry of the
+    // position map (pos[] is scratch here; it receives the seed's position in U at the end)
     extern __shared__ int64_t sh[];
     using BS = cub::BlockScan<int, 1024>;
     __shared__ typename BS::TempStorage tmp;
@@ -300,18 +302,19 @@ seeds_small_kernel(const int64_t* __restrict__ seeds, int n, int64_t N, int64_t*
         const bool ok = v >= 0 && v < N;
         if (!ok) atomicOr(err, 1);
         sh[i] = ok ? v : -1;
+        if (ok) pos[v] = 0x7fffffff;
     }
     if (threadIdx.x == 0) run = 0;
     __syncthreads();
+    for (int i = threadIdx.x; i < n; i += 1024)
+        if (sh[i] >= 0) atomicMin(&pos[sh[i]], i);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += 1024)      // keep flag: the sign bit of sh[i] (-1 = dropped)
+        if (sh[i] >= 0 && pos[sh[i]] != i) sh[i] = -1;
+    __syncthreads();
     for (int i0 = 0; i0 < n; i0 += 1024) {
         const int i = i0 + threadIdx.x;
-        bool keep = false;
-        if (i < n && sh[i] >= 0) {
-            keep = true;
-            const int64_t v = sh[i];
-            for (int j = 0; j < i; ++j)
-                if (sh[j] == v) { keep = false; break; }
-        }
+        const bool keep = i < n && sh[i] >= 0;
         int ex, agg;
         BS(tmp).ExclusiveSum((int)keep, ex, agg);
         if (keep) {
