@@ -101,7 +101,7 @@ def timed(fn, K):
 def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute", spread=False,
                      tune=False):
     """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
-    sampler (HBM-bound, 0.35 ms on the big partition) runs either in the training stream between
+    sampler (HBM-bound, ~0.3 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
     tuned = None
     if tune:   # measure a few partition shapes on this chip and keep the fastest (pipeline.tune_fetch_partition)

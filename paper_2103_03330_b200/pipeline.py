@@ -47,7 +47,7 @@ class MinibatchFetcher:
 
     Default (``sampler_sms=8``): the device is split with green contexts (``dgz.Partition``)
     into a small sampler group and a gather group, and the sampler of minibatch j+1 runs on its
-    8 SMs while minibatch j is gathered on the others -- the 0.36 ms of sampling disappears from
+    8 SMs while minibatch j is gathered on the others -- the ~0.3 ms of sampling disappears from
     the step (measured: 49.5 vs 46.6 GB/s).  Sampling on a second stream over the WHOLE GPU is
     much worse (27 GB/s: its full-GPU bitmap passes stall the translation-bound gather), so
     without green contexts (``sampler_sms=0``) both phases run back to back on one high-priority
