@@ -314,6 +314,21 @@ def run_ours(args, d: Dist):
     sm_count_all = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True,
                                sampler_sms=args.sampler_sms, graphs=args.graphs)
+    choice = None
+    if args.sampler_sms is None and not args.graphs and args.csr == "hbm" and fetcher.partition is not None:
+        # the pipeline's shape is picked by measurement on this box, before the timed region: on most
+        # boxes sampling on an 8-SM partition beside the gather is free, on some its DRAM traffic slows
+        # the gather's page walks more than the 0.3 ms of sampling it hides
+        alt = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True, sampler_sms=0)
+        t_p = calibrate(fetcher, seeds_dev, rng, W)
+        t_s = calibrate(alt, seeds_dev, rng, W)
+        choice = {"pipelined_ms_per_step": round(t_p, 3), "sequential_ms_per_step": round(t_s, 3)}
+        if t_s < t_p:
+            fetcher.close()
+            fetcher = alt
+        else:
+            alt.close()
+        choice["chosen"] = fetcher.mode
     cap = fetcher.bufs[0].bounds[-1]
     n_steps = torch.zeros(W + K, dtype=torch.int64, device="cuda")
     ceilings = measure_ceilings(dgz, d)
@@ -390,7 +405,7 @@ def run_ours(args, d: Dist):
                                f"{cfg.batch} seeds per GPU per step",
                    "global_batch": cfg.batch * G, "parallelism": f"dp{G} (seed partition j mod G)",
                    "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
-                   "pipeline": fetcher.mode,
+                   "pipeline": fetcher.mode, "pipeline_choice": choice,
                    "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else "pinned host memory, sampled by zero-copy",
                    "gather": dict(dgz.gather_plan(table, cap, True, gcfg),
                                   order="address-sorted + inverse permutation (dgz_gather_perm)")},
@@ -440,6 +455,22 @@ def run_ours(args, d: Dist):
 
 def pct(xs, q):
     return round(float(np.percentile(xs, q)), 4)
+
+
+def calibrate(fetcher, seeds_dev, rng, W, reps: int = 2):
+    """ms per step of `fetcher` over the warm-up minibatches (untimed setup; best of `reps` passes)."""
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(fetcher.sample_stream)
+        for i in range(W):
+            fetcher.fetch(seeds_dev[i], rng[i])
+        fetcher.stream.wait_stream(fetcher.sample_stream)
+        b.record(fetcher.stream)
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / W)
+    return best
 
 
 def run_latency(fetcher, cfg, seeds_dev, rng, n):
