@@ -283,7 +283,7 @@ def load_profile_traffic(cid):
 # ----------------------------------------------------------------------------------------------
 def run_ours(args, d: Dist):
     from paper_2103_03330_b200 import dgz
-    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher, calibrated_fetcher
 
     cfg = gen.CONFIGS[args.config]
     R = cfg.row_bytes
@@ -312,23 +312,15 @@ def run_ours(args, d: Dist):
     gcfg = (dgz.gather_cfg(sm_count=args.gather_sms, warps_per_cta=args.gather_warps, flags=gflags)
             if (args.gather_sms or args.gather_warps or gflags) else None)
     sm_count_all = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True,
-                               sampler_sms=args.sampler_sms, graphs=args.graphs)
     choice = None
-    if args.sampler_sms is None and not args.graphs and args.csr == "hbm" and fetcher.partition is not None:
-        # the pipeline's shape is picked by measurement on this box, before the timed region: on most
-        # boxes sampling on an 8-SM partition beside the gather is free, on some its DRAM traffic slows
-        # the gather's page walks more than the 0.3 ms of sampling it hides
-        alt = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True, sampler_sms=0)
-        t_p = calibrate(fetcher, seeds_dev, rng, W)
-        t_s = calibrate(alt, seeds_dev, rng, W)
-        choice = {"pipelined_ms_per_step": round(t_p, 3), "sequential_ms_per_step": round(t_s, 3)}
-        if t_s < t_p:
-            fetcher.close()
-            fetcher = alt
-        else:
-            alt.close()
-        choice["chosen"] = fetcher.mode
+    if args.sampler_sms is None and not args.graphs and args.csr == "hbm":
+        # the pipeline's shape is picked by measurement on the warm-up minibatches, before the timed
+        # region (pipeline.calibrated_fetcher)
+        fetcher, choice = calibrated_fetcher(table, graph, cfg.fanouts, cfg.batch, seeds_dev[:W], rng[:W], slots=2,
+                                             gather_cfg=gcfg, blocks=True)
+    else:
+        fetcher = MinibatchFetcher(table, graph, cfg.fanouts, cfg.batch, slots=2, gather_cfg=gcfg, blocks=True,
+                                   sampler_sms=args.sampler_sms, graphs=args.graphs)
     cap = fetcher.bufs[0].bounds[-1]
     n_steps = torch.zeros(W + K, dtype=torch.int64, device="cuda")
     ceilings = measure_ceilings(dgz, d)
@@ -455,22 +447,6 @@ def run_ours(args, d: Dist):
 
 def pct(xs, q):
     return round(float(np.percentile(xs, q)), 4)
-
-
-def calibrate(fetcher, seeds_dev, rng, W, reps: int = 2):
-    """ms per step of `fetcher` over the warm-up minibatches (untimed setup; best of `reps` passes)."""
-    best = float("inf")
-    for _ in range(reps):
-        torch.cuda.synchronize()
-        a, b = ev(), ev()
-        a.record(fetcher.sample_stream)
-        for i in range(W):
-            fetcher.fetch(seeds_dev[i], rng[i])
-        fetcher.stream.wait_stream(fetcher.sample_stream)
-        b.record(fetcher.stream)
-        torch.cuda.synchronize()
-        best = min(best, a.elapsed_time(b) / W)
-    return best
 
 
 def run_latency(fetcher, cfg, seeds_dev, rng, n):

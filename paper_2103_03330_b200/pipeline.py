@@ -261,3 +261,39 @@ def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds
         else:
             part.destroy()
     return best[0], best[1], results
+
+
+def _ms_per_fetch(f: MinibatchFetcher, seeds, rng_seeds, reps: int = 2) -> float:
+    """Steady-state ms per minibatch: from the end of the first gather to the end of the last (the
+    pipeline's fill -- the first, unhidden sampling -- is not charged to either shape)."""
+    assert len(seeds) >= 2
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f.fetch(seeds[0], rng_seeds[0])
+        a.record(f.stream)
+        for s, r in zip(seeds[1:], rng_seeds[1:]):
+            f.fetch(s, r)
+        b.record(f.stream)
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / (len(seeds) - 1))
+    return best
+
+
+def calibrated_fetcher(table: dgz.Table, graph, fanouts, max_seeds: int, seeds, rng_seeds, **kw):
+    """The default pipelined fetcher (sampler on an 8-SM green-context partition beside the gather) or
+    the sequential one (sample, then gather, on the whole GPU), whichever fetches the given sample
+    minibatches faster on THIS box: on most boxes the partitioned sampler is hidden for free, on some
+    its memory traffic slows the gather's page walks by more than the ~0.3 ms it hides (DESIGN.md
+    section 5).  Returns (fetcher, {"pipelined_ms_per_step", "sequential_ms_per_step", "chosen"});
+    the losing fetcher is closed."""
+    pipelined = MinibatchFetcher(table, graph, fanouts, max_seeds, **kw)
+    if pipelined.partition is None:
+        return pipelined, {"chosen": pipelined.mode, "note": "no green contexts: sequential only"}
+    sequential = MinibatchFetcher(table, graph, fanouts, max_seeds, **dict(kw, sampler_sms=0))
+    t_p = _ms_per_fetch(pipelined, seeds, rng_seeds)
+    t_s = _ms_per_fetch(sequential, seeds, rng_seeds)
+    keep, drop = (sequential, pipelined) if t_s < t_p else (pipelined, sequential)
+    drop.close()
+    return keep, {"pipelined_ms_per_step": round(t_p, 3), "sequential_ms_per_step": round(t_s, 3), "chosen": keep.mode}

@@ -706,3 +706,29 @@ def test_concurrent_streams(dev):
         dgz.check_errors(t.table)
     finally:
         t.close()
+
+
+def test_calibrated_fetcher(dev):
+    """pipeline.calibrated_fetcher times the pipelined and the sequential fetcher and keeps the faster;
+    its minibatches equal the oracle's."""
+    from paper_2103_03330_b200.pipeline import calibrated_fetcher
+    c = gen.CONFIGS[1]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    t = HostTable(c.n_nodes, c.row_bytes, seed=c.seed, dtype=dgz.F32)
+    try:
+        g = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+        seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in range(3)]
+        rs = [gen.batch_rng_seed(c.seed, j) for j in range(3)]
+        f, choice = calibrated_fetcher(t.table, g, c.fanouts, c.batch, seeds, rs)
+        assert choice["chosen"] == f.mode
+        for j in (4, 5):
+            seeds_np = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
+            mb = f.fetch(torch.from_numpy(seeds_np).cuda(), gen.batch_rng_seed(c.seed, j))
+            n = mb.sizes()[-1]
+            want = oracle.sample_uniform(off, col, seeds_np, c.fanouts, gen.batch_rng_seed(c.seed, j), with_blocks=False)
+            exp, _ = oracle.gather(t.np, c.row_bytes, want.U)
+            assert np.array_equal(mb.bufs.ids[:n].cpu().numpy(), want.U)
+            assert np.array_equal(mb.rows[:n].cpu().numpy(), exp)
+        f.close()
+    finally:
+        t.close()
