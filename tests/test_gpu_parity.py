@@ -732,3 +732,26 @@ def test_calibrated_fetcher(dev):
         f.close()
     finally:
         t.close()
+
+
+def test_gather_plan_reports_table_kind_defaults(dev):
+    """dgz_gather_plan: HBM-resident tables get 8 warps x 8 CTAs per SM; a host table's unsorted
+    gather 16 warps; explicit configs are passed through."""
+    nsm = dgz.device_sm_count()
+    dev_rows = torch.empty(1000 * 512, dtype=torch.uint8, device="cuda")
+    dt = dgz.DeviceTable(dev_rows.data_ptr(), 1000, 128, dgz.F32)
+    try:
+        p = dgz.gather_plan(dt, 1_000_000, False)
+        assert (p["sm_count"], p["warps_per_cta"]) == (nsm, 8) and p["ctas"] == nsm * 8
+        p = dgz.gather_plan(dt, 100_000, False)       # small lists: no more CTAs than 8-warp batches
+        assert p["ctas"] == -(-(-(-100_000 // 32)) // 8)
+    finally:
+        dt.unregister()
+    t = HostTable(1000, 512, seed=1, dtype=dgz.F32)
+    try:
+        p = dgz.gather_plan(t.table, 100_000, False)
+        assert (p["sm_count"], p["warps_per_cta"], p["line_loads_per_lane"]) == (nsm, 16, 8)
+        p = dgz.gather_plan(t.table, 100_000, True, dgz.gather_cfg(sm_count=12, warps_per_cta=4, flags=dgz.FLAG_DYNAMIC))
+        assert (p["sm_count"], p["warps_per_cta"], p["schedule"]) == (12, 4, "work counter")
+    finally:
+        t.close()
