@@ -374,7 +374,8 @@ def run_ours(args, d: Dist):
     lat = run_latency(fetcher, cfg, seeds_dev, rng, min(K, 16))
 
     # ---- overlap with a stand-in consumer (steps a5-a7)
-    overlap = run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K) if (args.overlap and rank == 0) else None
+    overlap = (run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args.overlap_warps)
+               if (args.overlap and rank == 0) else None)
 
     # ---- baselines (rank 0 only, N=1 at most the box's cores): oracle + CPU-gather+memcpy
     cpu_base = dma_base = parity = None
@@ -503,7 +504,7 @@ def run_e2e(fetcher, cfg, seeds_host, rng, W, K, d: Dist):
                    "behind), wall clock"}
 
 
-def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
+def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, overlap_warps=0):
     """Exposed fetch time with a stand-in GraphSAGE mean-aggregation consumer (a5-a7) and the
     SM-partition sweep (a6; the B200 analogue of the paper's MPS ratio sweep, fig:mps_bandwidth):
     the fetch runs on a green-context partition of k SMs (dgz_partition, spread over the GPCs),
@@ -574,7 +575,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
     # partition shapes: k SMs spread over every GPC, or k contiguous SMs of the split (DESIGN 5:
     # the gather's rate depends strongly and reproducibly on WHICH SMs it gets, explore25)
     for k, pflags in ((8, dgz.PARTITION_SPREAD), (16, dgz.PARTITION_SPREAD), (24, dgz.PARTITION_SPREAD),
-                      (8, 0), (16, 0), (24, 0)):
+                      (32, dgz.PARTITION_SPREAD), (16, 0), (24, 0)):
         try:
             part = dgz.Partition(k, -1, pflags)
         except Exception as e:  # green contexts unavailable: report and skip
@@ -582,8 +583,10 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
             continue
         shape = "spread over the GPCs" if pflags else "contiguous"
         # grid sized to the partition: one 8-warp CTA per SM, 16 line loads per lane (explore15)
-        # work-counter batches: a partition's slower SMs take fewer batches (explore28)
-        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
+        # work-counter batches (a partition's slower SMs take fewer batches, explore28) and few warps
+        # per SM: beside a DRAM-heavy consumer the page walks slow down and fewer rows in flight win
+        w = overlap_warps or max(2, 64 // part.fetch_sms)   # ~64 warps in all (8 SMs x 8 ... 32 SMs x 2)
+        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=w, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
         # sampler placement: in front of the gather on the small partition, or in the consumer's stream
         # between consumer steps (its full-partition bitmap passes then run beside the gather and slow
         # its page walks, but it leaves the small partition; DESIGN 5) -- both measured
@@ -592,6 +595,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
                                  gather_cfg=pcfg, sample_stream=part.compute_stream if where == "consumer stream" else None)
             t_g, t_c, t_o, _ = measure(f, part.compute_stream, repeat=repeat)
             rows.append({"partition": f"green context ({shape}), sampler in the {where}", "fetch_sms": part.fetch_sms,
+                         "warps_per_sm": w,
                          "compute_sms": part.compute_sms,
                          "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
                          "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
@@ -602,7 +606,9 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K):
     best = min((r for r in rows if "t_step_overlapped_ms" in r), key=lambda r: r["t_step_overlapped_ms"])
     return {"t_fetch_ms": round(t_g0, 3), "consumer_repeat": repeat, "serial_ms": round(t_g0 + t_c0, 3), "best": best,
             "hidden_frac_best": round(1 - best["exposed_fetch_ms"] / t_g0, 3), "sweep": rows,
-            "consumer": "dgz_aggregate_mean over the last hop's block, non-persistent launches, repeated to T_c ~ T_fetch"}
+            "consumer": "dgz_aggregate_mean over the last hop's block, non-persistent launches, repeated to T_c ~ T_fetch",
+            "partition_gather": (f"{overlap_warps} warps per SM" if overlap_warps else "max(2, 64 / SMs) warps per SM")
+                                + ", 16 loads per lane, work-counter batches"}
 
 
 def run_oracle_leg(cfg, table_addr, off, col, last, d: Dist, budget: float = 20.0):
@@ -740,6 +746,8 @@ def main():
     ap.add_argument("--csr", default="hbm", choices=["hbm", "host"],
                     help="CSR replicated in HBM (default) or left in pinned host memory and sampled by zero-copy")
     ap.add_argument("--dynamic", action="store_true", help="gather batches from a work counter (DGZ_GATHER_FLAG_DYNAMIC)")
+    ap.add_argument("--overlap-warps", type=int, default=0,
+                    help="warps per SM of the overlap sweep's partition gathers (0: ~64 warps in all, at least 2 per SM)")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false")
     args = ap.parse_args()

@@ -16,7 +16,7 @@ The model is plain PyTorch (mean-aggregator SAGE layers): it is not t
 fetch is.  The table holds random bytes, not meaningful features: inputs are clamped to finite
 values, labels are synthetic (seed ID mod classes).
 
-    python examples/graphsage_train.py [--config 4] [--steps 20] [--modes zc,dma,hbm] [--fetch-sms 16]
+    python examples/graphsage_train.py [--config 4] [--steps 20] [--modes zc,dma,hbm] [--fetch-sms 32] [--fetch-warps 2] [--contiguous] [--tune]
     torchrun --nproc-per-node N examples/graphsage_train.py --modes zc,dma     (DDP, one process per GPU)
 
 Prints one JSON line: per mode the pipelined step time, the training time alone, and speedups.
@@ -99,7 +99,7 @@ def timed(fn, K):
 
 
 def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute", spread=False,
-                     tune=False):
+                     tune=False, fetch_warps=8):
     """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
     sampler (HBM-bound, ~0.3 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
@@ -109,7 +109,7 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
         part, pcfg, tuned = tune_fetch_partition(table, graph, c.fanouts, c.batch, seeds[:4], rng[:4])
     else:
         part = dgz.Partition(fetch_sms, -1, dgz.PARTITION_SPREAD if spread else 0)
-        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=8, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
+        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=fetch_warps, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
     comp = part.compute_stream
     f = MinibatchFetcher(table, graph, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=pcfg,
                          sample_stream=comp if sample_on == "compute" else None)
@@ -149,6 +149,7 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
            "exposed_fetch_ms": round(max(0.0, t_pipe - t_train), 3), "loss": round(float(loss), 4),
            "fetch_sms": part.fetch_sms, "train_sms": part.compute_sms, "sampler_on": sample_on,
            "fetch_partition": ("tuned: " + json.dumps(tuned)) if tuned else ("spread over the GPCs" if spread else "contiguous"),
+           "fetch_warps_per_sm": pcfg.warps_per_cta,
            "rows_per_minibatch": sz[-1]}
     f.close()
     torch.cuda.synchronize()
@@ -243,10 +244,13 @@ def main():
     ap.add_argument("--hidden", type=int, default=256)
     ap.add_argument("--classes", type=int, default=172)      # ogbn-papers100M has 172 classes
     ap.add_argument("--modes", default="zc,dma,hbm")
-    ap.add_argument("--fetch-sms", type=int, default=16)
+    ap.add_argument("--fetch-sms", type=int, default=32)
     ap.add_argument("--sample-on", default="compute", choices=["compute", "fetch"])
-    ap.add_argument("--spread", action="store_true", help="fetch SMs spread over the GPCs (default: contiguous)")
+    ap.add_argument("--contiguous", dest="spread", action="store_false",
+                    help="fetch SMs contiguous in the split (default: spread over the GPCs)")
     ap.add_argument("--tune", action="store_true", help="time a few fetch partitions first and keep the fastest")
+    ap.add_argument("--fetch-warps", type=int, default=2,
+                    help="warps per SM of the partition's gather (few: beside training the page walks slow down)")
     ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))   # one core left for the training loop
     a = ap.parse_args()
     # one process per GPU under torchrun (DDP; DGZ_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 with gloo)
@@ -293,7 +297,8 @@ def main():
     threads = max(1, a.threads // G)
     if "zc" in modes:
         res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms,
-                                     lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune)
+                                     lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune,
+                                     a.fetch_warps)
     if "dma" in modes:
         host_rows = torch.from_numpy(buf.numpy(0, c.table_bytes)).view(c.n_nodes, c.row_bytes)
         res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, Trainer(c, a.hidden, a.classes, G > 1))
@@ -302,7 +307,8 @@ def main():
         dev.copy_(torch.from_numpy(buf.numpy(0, c.table_bytes)))
         dtab = dgz.DeviceTable(dev.data_ptr(), c.n_nodes, c.dim, dgz.F32)
         res["hbm"] = run_fetcher_mode(dtab, graph, c, seeds, rng, K, a.fetch_sms,
-                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune)
+                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune,
+                                     a.fetch_warps)
         dtab.unregister()
         del dev
     if G > 1:   # per-rank results to rank 0; the job's step time is the slowest rank's

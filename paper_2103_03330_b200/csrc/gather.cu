@@ -509,6 +509,20 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
         const int sw = (int)(x & (~x + 1));
         unsigned long long* ctr = nullptr;
         if (flags & DGZ_GATHER_FLAG_DYNAMIC) {
+            // the 8-byte counter comes from the device's stream-ordered pool; keep the pool's memory
+            // reserved across synchronisations (release threshold) so that a fetch loop that syncs
+            // every step does not map fresh memory for each launch
+            static int pool_tuned[64] = {0};
+            int devn = 0;
+            cudaGetDevice(&devn);
+            if (devn >= 0 && devn < 64 && !pool_tuned[devn]) {
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, devn) == cudaSuccess) {
+                    uint64_t thr = uint64_t(64) << 20;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
+                pool_tuned[devn] = 1;
+            }
             DGZ_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), s));
             DGZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
         }

@@ -216,17 +216,18 @@ def _as_i64(x: int) -> int:
 
 
 def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds, rng_seeds, candidates=None,
-                         warps_per_cta: int = 8):
+                         warps_per_cta: int = 2):
     """Pick the green-context partition whose SMs gather fastest on THIS chip (DESIGN.md section 5:
     at a fixed SM count the zero-copy gather's rate depends strongly and reproducibly on which SMs
     walk the GPU page tables, and the best set differs between chips).  Samples the given minibatches
     once, then times the address-sorted gather of all of them on each candidate partition (alone)
     and returns (best dgz.Partition, its gather config, [(candidate, GB/s), ...]); the other
     partitions are destroyed.  candidates: list of dicts with either {"sms": k, "flags": f} or
-    {"groups": [...]} (dgz_partition_create_groups); default: 16 and 24 SMs, contiguous and spread."""
+    {"groups": [...]} (dgz_partition_create_groups); default: 24 and 32 SMs, contiguous and spread, with
+    2 warps per SM (few rows in flight: the page walks are what the gather waits on)."""
     if candidates is None:
-        candidates = [{"sms": 16, "flags": 0}, {"sms": 16, "flags": dgz.PARTITION_SPREAD},
-                      {"sms": 24, "flags": 0}, {"sms": 24, "flags": dgz.PARTITION_SPREAD}]
+        candidates = [{"sms": 24, "flags": 0}, {"sms": 24, "flags": dgz.PARTITION_SPREAD},
+                      {"sms": 32, "flags": 0}, {"sms": 32, "flags": dgz.PARTITION_SPREAD}]
     fanouts = tuple(int(f) for f in fanouts)
     L = len(fanouts)
     bufs = []

@@ -1,7 +1,7 @@
 # training step with the fetch on contiguous vs spread partitions (examples/graphsage_train.py)
 for s in 16 24; do
+  python examples/graphsage_train.py --modes zc --fetch-sms $s --steps 20 --contiguous >> gpurun_out/train_spread.jsonl 2>>gpurun_out/train_spread.err
   python examples/graphsage_train.py --modes zc --fetch-sms $s --steps 20 >> gpurun_out/train_spread.jsonl 2>>gpurun_out/train_spread.err
-  python examples/graphsage_train.py --modes zc --fetch-sms $s --steps 20 --spread >> gpurun_out/train_spread.jsonl 2>>gpurun_out/train_spread.err
 done
 python bench.py --no-baselines --steps 20 > gpurun_out/bench_ov3.json 2>gpurun_out/bench_ov3.err
 python - <<'PY'
