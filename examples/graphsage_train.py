@@ -104,9 +104,18 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
     sampler (HBM-bound, ~0.3 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
     tuned = None
-    if tune:   # measure a few partition shapes on this chip and keep the fastest (pipeline.tune_fetch_partition)
+    if tune:   # time a few partition shapes UNDER training load on this chip and keep the fastest
         from paper_2103_03330_b200.pipeline import tune_fetch_partition
-        part, pcfg, tuned = tune_fetch_partition(table, graph, c.fanouts, c.batch, seeds[:4], rng[:4])
+        probe = make_trainer()          # a throw-away model: the consumer the candidates are timed beside
+
+        def consumer(mb, stream):
+            sz = mb.sizes()
+            with torch.cuda.stream(stream):
+                probe.step(mb.rows, mb.bufs, sz)
+        cands = [{"sms": k, "flags": dgz.PARTITION_SPREAD, "warps": w} for k, w in ((16, 3), (24, 2), (32, 2), (32, 3), (24, 8))]
+        part, pcfg, tuned = tune_fetch_partition(table, graph, c.fanouts, c.batch, seeds[:6], rng[:6], candidates=cands,
+                                                 consumer=consumer)
+        del probe
     else:
         part = dgz.Partition(fetch_sms, -1, dgz.PARTITION_SPREAD if spread else 0)
         pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=fetch_warps, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)

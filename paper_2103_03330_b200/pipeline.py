@@ -216,15 +216,20 @@ def _as_i64(x: int) -> int:
 
 
 def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds, rng_seeds, candidates=None,
-                         warps_per_cta: int = 2):
+                         warps_per_cta: int = 2, consumer=None):
     """Pick the green-context partition whose SMs gather fastest on THIS chip (DESIGN.md section 5:
     at a fixed SM count the zero-copy gather's rate depends strongly and reproducibly on which SMs
     walk the GPU page tables, and the best set differs between chips).  Samples the given minibatches
     once, then times the address-sorted gather of all of them on each candidate partition (alone)
     and returns (best dgz.Partition, its gather config, [(candidate, GB/s), ...]); the other
     partitions are destroyed.  candidates: list of dicts with either {"sms": k, "flags": f} or
-    {"groups": [...]} (dgz_partition_create_groups); default: 24 and 32 SMs, contiguous and spread, with
-    2 warps per SM (few rows in flight: the page walks are what the gather waits on)."""
+    {"groups": [...]} (dgz_partition_create_groups), optionally with "warps"; default: 24 and 32 SMs,
+    contiguous and spread, with 2 warps per SM (few rows in flight: the page walks are what the gather
+    waits on).  With ``consumer(minibatch, stream)`` -- e.g. one training step enqueued on `stream` --
+    each candidate is instead timed UNDER LOAD: the fetch of step j+1 on the partition while the
+    consumer works on step j on the other SMs, which is the shape that matters in training (the
+    consumer's DRAM traffic slows the gather's page walks).  Results are then
+    ms per pipelined step (lower is better) instead of GB/s."""
     if candidates is None:
         candidates = [{"sms": 24, "flags": 0}, {"sms": 24, "flags": dgz.PARTITION_SPREAD},
                       {"sms": 32, "flags": 0}, {"sms": 32, "flags": dgz.PARTITION_SPREAD}]
@@ -241,7 +246,18 @@ def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds
     results, best = [], None
     for cand in candidates:
         part = dgz.Partition(cand.get("sms", 0), -1, cand.get("flags", 0), groups=cand.get("groups"))
-        cfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=warps_per_cta, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
+        cfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=cand.get("warps", warps_per_cta),
+                             flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
+        if consumer is not None:
+            ms = _ms_per_loaded_step(table, graph, fanouts, max_seeds, seeds, rng_seeds, part, cfg, consumer)
+            results.append((dict(cand, fetch_sms=part.fetch_sms), round(ms, 3)))
+            if best is None or ms < best[2]:
+                if best is not None:
+                    best[0].destroy()
+                best = (part, cfg, ms)
+            else:
+                part.destroy()
+            continue
         s = part.fetch_stream
         b0 = bufs[0]
         dgz.gather_perm(table, b0.ids_sorted, b0.ids_sorted_pos, out, n=b0.bounds[-1], n_dev=b0.sizes_dev[L:L + 1],
@@ -262,6 +278,30 @@ def tune_fetch_partition(table: dgz.Table, graph, fanouts, max_seeds: int, seeds
         else:
             part.destroy()
     return best[0], best[1], results
+
+
+def _ms_per_loaded_step(table, graph, fanouts, max_seeds, seeds, rng_seeds, part, cfg, consumer) -> float:
+    """ms per pipelined step: fetch j+1 on the partition (sampler in the consumer's stream) while the
+    consumer works on step j on the other SMs (second of two passes)."""
+    import time
+    f = MinibatchFetcher(table, graph, fanouts, max_seeds, fetch_stream=part.fetch_stream, gather_cfg=cfg,
+                         sample_stream=part.compute_stream)
+    comp = part.compute_stream
+    out = 0.0
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cur = f.fetch(seeds[0], rng_seeds[0])
+        for i in range(1, len(seeds) + 1):
+            nxt = f.fetch(seeds[i], rng_seeds[i]) if i < len(seeds) else None
+            comp.wait_event(cur.event)
+            consumer(cur, comp)
+            f.release(cur, comp)
+            cur = nxt
+        torch.cuda.synchronize()
+        out = (time.perf_counter() - t0) * 1e3 / len(seeds)
+    f.close()
+    return out
 
 
 def _ms_per_fetch(f: MinibatchFetcher, seeds, rng_seeds, reps: int = 2) -> float:
