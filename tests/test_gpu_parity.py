@@ -618,6 +618,16 @@ def test_tune_fetch_partition_then_fetch(dev):
         part, cfg, res = tune_fetch_partition(t.table, g, c.fanouts, c.batch, seeds, rs, candidates=cands)
         assert len(res) == 2 and all(gbs > 0 for _, gbs in res)
         assert part.fetch_sms in (r[0]["fetch_sms"] for r in res)
+        part.destroy()
+        # under load: a stand-in consumer (a few HBM passes over the rows) on the compute SMs
+
+        def consumer(mb, stream):
+            with torch.cuda.stream(stream):
+                for _ in range(4):
+                    mb.rows.float().sum()
+        part, cfg, res = tune_fetch_partition(t.table, g, c.fanouts, c.batch, seeds, rs,
+                                              candidates=[dict(x, warps=2) for x in cands], consumer=consumer)
+        assert len(res) == 2 and all(ms > 0 for _, ms in res) and cfg.warps_per_cta == 2
         f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=cfg)
         seeds_np = gen.batch_seeds(c.n_nodes, c.batch, c.seed, 5)
         mb = f.fetch(torch.from_numpy(seeds_np).cuda(), gen.batch_rng_seed(c.seed, 5))
