@@ -122,7 +122,8 @@ class MinibatchFetcher:
 
     def fetch(self, seeds: torch.Tensor, rng_seed: int, slot: int | None = None, timing: bool = False,
               count_into: torch.Tensor | None = None) -> Minibatch:
-        """Enqueue sampling + gather of one minibatch (seeds: int64, on the device or pinned host).
+        """Enqueue sampling + gather of one minibatch (seeds: int64, on the device or pinned host; a
+        host tensor is copied asynchronously, so keep it unchanged until the minibatch's event).
         ``count_into``: a 1-element device int64 tensor that receives |U| on the gather stream."""
         p = self.next_slot if slot is None else slot
         self.next_slot = (p + 1) % len(self.bufs)
