@@ -335,6 +335,7 @@ def run_ours(args, d: Dist):
     d.barrier()
     torch.cuda.synchronize()
     launches0 = dgz.kernel_launches()
+    replays0 = fetcher.graph_replays
     t_start, t_end = ev(), ev()
     with ClockSampler(d.local) as clk:
         t_start.record(fetcher.sample_stream)
@@ -343,7 +344,8 @@ def run_ours(args, d: Dist):
         fetcher.stream.wait_stream(fetcher.sample_stream)
         t_end.record(fetcher.stream)
         torch.cuda.synchronize()
-    launches = dgz.kernel_launches() - launches0
+    # kernels launched by libdgz calls, plus those replayed inside CUDA graphs (--graphs)
+    launches = dgz.kernel_launches() - launches0 + (fetcher.graph_replays - replays0) * fetcher.graph_kernels
     d.barrier()
     torch.cuda.synchronize()
     dgz.check_errors(table)

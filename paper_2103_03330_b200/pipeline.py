@@ -99,6 +99,8 @@ class MinibatchFetcher:
         self.bufs = [dgz.SampleBuffers(graph.n_nodes, max_seeds, self.fanouts, blocks=blocks, local=blocks,
                                        sorted_ids=True, device_rng=graphs) for _ in range(slots)]
         self.cuda_graphs = [None] * slots
+        self.graph_kernels = 0     # libdgz kernels per graph replay (counted at capture)
+        self.graph_replays = 0
         if graphs:
             self.mode = "sequential, one CUDA graph per slot (sampler + gather replayed as one launch)"
         cap = self.bufs[0].bounds[-1]
@@ -190,8 +192,10 @@ class MinibatchFetcher:
                 self._enqueue_graph_body(p)
             s.synchronize()
             g = torch.cuda.CUDAGraph()
+            k0 = dgz.kernel_launches()
             with torch.cuda.graph(g, stream=s):
                 self._enqueue_graph_body(p)
+            self.graph_kernels = dgz.kernel_launches() - k0   # libdgz kernels captured per replay
             self.cuda_graphs[p] = g
         with torch.cuda.stream(s):
             if ev:
@@ -201,6 +205,7 @@ class MinibatchFetcher:
             if ev:
                 ev[1].record(s)
             self.cuda_graphs[p].replay()
+            self.graph_replays += 1
             if ev:
                 ev[2].record(s)
             if count_into is not None:
