@@ -20,6 +20,8 @@
 // NAIVE / SHIFT kernels: the paper's Listing 2 without / with the circular shift stage, one
 // element per thread (ablations for the fig:alignment_measurement analogue).  The shift
 // aligns to 128 BYTES (W = 128 / sizeof(T) elements; reading R3) with 64-bit offsets (R4).
+#include <atomic>
+
 #include "internal.h"
 
 namespace {
@@ -512,16 +514,15 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
             // the 8-byte counter comes from the device's stream-ordered pool; keep the pool's memory
             // reserved across synchronisations (release threshold) so that a fetch loop that syncs
             // every step does not map fresh memory for each launch
-            static int pool_tuned[64] = {0};
+            static std::atomic<int> pool_tuned[64];
             int devn = 0;
             cudaGetDevice(&devn);
-            if (devn >= 0 && devn < 64 && !pool_tuned[devn]) {
+            if (devn >= 0 && devn < 64 && !pool_tuned[devn].exchange(1)) {   // once per device, any thread
                 cudaMemPool_t pool;
                 if (cudaDeviceGetDefaultMemPool(&pool, devn) == cudaSuccess) {
                     uint64_t thr = uint64_t(64) << 20;
                     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
                 }
-                pool_tuned[devn] = 1;
             }
             DGZ_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), s));
             DGZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
