@@ -89,17 +89,20 @@ def gen_csr(n: int, avg_degree: float, seed: int, col_dtype=np.int32, skew_alpha
     return off, col
 
 
-def gen_csr_into(n: int, avg_degree: float, seed: int, alloc):
-    """gen_csr (int32 columns, uniform endpoints) written into caller memory: ``alloc(nbytes)``
-    returns a writable address (e.g. a shared /dev/shm mapping one rank fills for all).  Returns
-    (offsets address, cols address, n_edges); the bytes equal gen_csr's."""
+def gen_csr_into(n: int, avg_degree: float, seed: int, alloc, skew_alpha: float = 0.0):
+    """gen_csr (int32 columns) written into caller memory: ``alloc(nbytes)`` returns a writable
+    address (e.g. a shared /dev/shm mapping one rank fills for all).  Returns (offsets address,
+    cols address, n_edges); the bytes equal gen_csr's with the same skew_alpha."""
     assert n < 2**31
     po = int(alloc((n + 1) * 8))
     e = lib().dgz_gen_offsets(n, float(avg_degree), seed, po)
     if e < 0:
         raise ValueError("bad graph parameters")
     pc = int(alloc(max(e * 4, 1)))
-    lib().dgz_gen_cols32(n, e, seed, pc)
+    if skew_alpha > 1.0:
+        lib().dgz_gen_cols32_skewed(n, e, seed, float(skew_alpha), pc)
+    else:
+        lib().dgz_gen_cols32(n, e, seed, pc)
     return po, pc, int(e)
 
 
@@ -136,6 +139,30 @@ def distinct_ids(rows: int, n: int, seed: int) -> np.ndarray:
     out = np.empty(n, dtype=np.int64)
     lib().dgz_gen_distinct_ids(rows, n, seed, _ptr(out))
     return out
+
+
+def adjacent_run_ids(rows: int, n: int, seed: int, max_run: int = 8) -> np.ndarray:
+    """n IDs made of runs of 1..max_run table-adjacent rows (start uniform), plus a few repeats,
+    in shuffled run order: the dense lists whose sorted order puts neighbouring rows side by side
+    (two rows sharing a 128 B line), as a dense minibatch does."""
+    rng = np.random.default_rng(seed)
+    parts, got = [], 0
+    while got < n:
+        k = int(rng.integers(1, max_run + 1))
+        s = int(rng.integers(0, max(rows - k, 1)))
+        run = np.arange(s, min(s + k, rows), dtype=np.int64)
+        parts.append(run)
+        got += run.shape[0]
+    ids = np.concatenate(parts)[:n]
+    if n > 16:   # duplicates
+        j = rng.integers(0, n, size=max(1, n // 64))
+        ids[rng.integers(0, n, size=j.shape[0])] = ids[j]
+    return ids
+
+
+def float_table(count: int, seed: int) -> np.ndarray:
+    """count finite fp32 values, uniform in [-1, 1) (for consumers that do arithmetic on rows)."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=count).astype(np.float32)
 
 
 def rank_batches(rank: int, world: int, steps: int, start: int = 0):

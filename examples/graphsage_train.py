@@ -98,8 +98,18 @@ def timed(fn, K):
     return (time.perf_counter() - t0) * 1e3 / K, r
 
 
+def dump_minibatch(path, j, ids, rows, blocks=None):
+    """Write one fetched minibatch (global batch j: U, its rows, per-hop counts / positions in U) to an
+    .npz file, so that a test can check what the training consumed against the CPU oracle."""
+    d = {"j": np.int64(j), "U": ids.cpu().numpy(), "rows": rows.cpu().numpy()}
+    for k, (cnt, loc) in enumerate(blocks or []):
+        d[f"cnt{k}"] = cnt.cpu().numpy()
+        d[f"loc{k}"] = loc.cpu().numpy()
+    np.savez(path, **d)
+
+
 def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute", spread=False,
-                     tune=False, fetch_warps=8):
+                     tune=False, fetch_warps=8, dump=None):
     """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
     sampler (HBM-bound, ~0.3 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
@@ -134,6 +144,10 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
     t_fetch, _ = timed(fetch_alone, K)
     mb = f.fetch(seeds[0], rng[0])
     sz = mb.sizes()
+    if dump:   # (path, j): the minibatch every timed loop starts with, as the model sees it
+        n = sz[-1]
+        dump_minibatch(dump[0], dump[1], mb.bufs.ids[:n], mb.rows[:n],
+                       [(cnt, loc) for (nbr, cnt, loc) in mb.bufs.hop_blocks(sz)])
     with torch.cuda.stream(comp):
         for _ in range(2):
             trainer.step(mb.rows, mb.bufs, sz)
@@ -166,7 +180,7 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
     return out
 
 
-def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
+def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer, dump=None):
     """The paper's DMA-based method, pipelined: a worker thread samples on the GPU,
     copies U to the host, gathers the rows with `threads` CPU threads into pinned staging and
     copies them H2D; the main thread trains on the previous minibatch meanwhile."""
@@ -240,9 +254,44 @@ def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer):
                 rows[p][:n].copy_(stage[p][:n], non_blocking=True)
         s_fetch.synchronize()
     t_fetch, _ = timed(fetch_alone, K)
+    if dump:   # the last minibatch fetch_alone staged: slot (K-1) % 2, global batch dump[1]
+        p = (K - 1) % 2
+        n = int(bufs[p].sizes_host[-1])
+        dump_minibatch(dump[0], dump[1], ids_h[p][:n], rows[p][:n])
     t_pipe, loss = timed(lambda: loop(0, K), K)
     return {"step_ms": round(t_pipe, 3), "fetch_alone_ms": round(t_fetch, 3), "cpu_gather_ms": round(1e3 * float(np.median(t_cpu)), 3),
             "cpu_threads": threads, "loss": round(float(loss), 4)}
+
+
+def load_graph(c, G, rank, dist):
+    """The CSR in this GPU's HBM.  With G > 1 ranks rank 0 generates it once into /dev/shm and every
+    rank maps it (one host copy per box, as for the table) before uploading its own HBM copy."""
+    if G == 1:
+        off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+        return dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+    base = f"/dgz_train_csr_{os.environ.get('MASTER_PORT', '0')}"
+    bufs = []
+    e = [None]
+    if rank == 0:
+        def alloc(nb):
+            b = dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{len(bufs)}", create=True)
+            bufs.append(b)
+            return b.ptr
+        _, _, e[0] = gen.gen_csr_into(c.n_nodes, c.avg_degree, c.seed, alloc)
+    dist.broadcast_object_list(e, src=0)
+    if rank != 0:
+        for i, nb in enumerate(((c.n_nodes + 1) * 8, max(e[0] * 4, 1))):
+            bufs.append(dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{i}", create=False))
+    dist.barrier()
+    off = torch.from_numpy(bufs[0].numpy(0, (c.n_nodes + 1) * 8).view(np.int64)).cuda()
+    col = torch.from_numpy(bufs[1].numpy(0, e[0] * 4).view(np.int32)).cuda()
+    dist.barrier()
+    if rank == 0:
+        for b in bufs:
+            b.unlink()
+    for b in bufs:
+        b.free()
+    return dgz.Graph(off, col)
 
 
 def main():
@@ -261,6 +310,8 @@ def main():
     ap.add_argument("--fetch-warps", type=int, default=2,
                     help="warps per SM of the partition's gather (few: beside training the page walks slow down)")
     ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))   # one core left for the training loop
+    ap.add_argument("--dump", default=None,
+                    help="directory: write the first zc minibatch and the last DMA minibatch of each rank as .npz")
     a = ap.parse_args()
     # one process per GPU under torchrun (DDP; DGZ_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 with gloo)
     G = int(os.environ.get("WORLD_SIZE", "1"))
@@ -293,9 +344,7 @@ def main():
         if rank == 0:
             buf.unlink()
     table = dgz.register_table(buf.ptr, c.n_nodes, c.dim, dgz.F32)
-    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
-    graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
-    del off, col
+    graph = load_graph(c, G, rank, dist)
     batches = [i * G + rank for i in range(K + 2)]          # seed partition: global batch j = i*G + rank
     seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in batches]
     rng = [gen.batch_rng_seed(c.seed, j) for j in batches]
@@ -304,13 +353,17 @@ def main():
                                                               + (", DDP" if G > 1 else "")}
     modes = a.modes.split(",")
     threads = max(1, a.threads // G)
+    if a.dump:
+        os.makedirs(a.dump, exist_ok=True)
     if "zc" in modes:
         res["zc"] = run_fetcher_mode(table, graph, c, seeds, rng, K, a.fetch_sms,
                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune,
-                                     a.fetch_warps)
+                                     a.fetch_warps,
+                                     dump=(os.path.join(a.dump, f"zc_rank{rank}.npz"), batches[0]) if a.dump else None)
     if "dma" in modes:
         host_rows = torch.from_numpy(buf.numpy(0, c.table_bytes)).view(c.n_nodes, c.row_bytes)
-        res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, Trainer(c, a.hidden, a.classes, G > 1))
+        res["dma"] = run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, Trainer(c, a.hidden, a.classes, G > 1),
+                                  dump=(os.path.join(a.dump, f"dma_rank{rank}.npz"), batches[K - 1]) if a.dump else None)
     if "hbm" in modes:
         dev = torch.empty(c.table_bytes, dtype=torch.uint8, device="cuda")
         dev.copy_(torch.from_numpy(buf.numpy(0, c.table_bytes)))

@@ -114,8 +114,12 @@ DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 /* host_ptr: row 0 of a row-major, unpadded rows x dim table of `dtype` elements in host
  * memory (any alignment; unaligned bases are a first-class case, S:37 base_offset).  The caller
  * owns the memory and must keep it alive and unmodified-in-size until dgz_unregister_table.
- * Registers on the CURRENT device.  rows >= 1, dim >= 1.  Pages shared with another
- * registration are accepted (already-registered pages are mapped, not re-pinned). */
+ * Registers on the CURRENT device.  rows >= 1, dim >= 1.  A span whose pages are ALL already
+ * registered (by another table or by the caller) is mapped, not re-pinned; a span that only
+ * partly overlaps an existing registration (e.g. two tables sharing a boundary page) is refused
+ * with DGZ_ERR_STATE, because cudaHostRegister cannot extend a registration (probed at the first
+ * and last byte and every 64 MiB between).  A DGZ_REG_VMM_BACKED table is granted to another
+ * device on that device's first gather. */
 DGZ_API dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int64_t dim, dgz_dtype dtype,
                               uint32_t flags, dgz_table* out);
 DGZ_API dgz_status dgz_unregister_table(dgz_table t);
@@ -187,7 +191,10 @@ typedef struct {
 #define DGZ_GATHER_FLAG_EVICT_FIRST_LOADS 16 /* SEGMENT: zero-copy loads under an L2 evict_first policy */
 #define DGZ_GATHER_FLAG_DYNAMIC 32       /* SEGMENT: warps take 32-row batches from a work counter (in
                                             ascending order) instead of a static interleave; the 8-byte
-                                            counter comes from the stream-ordered pool (cudaMallocAsync) */
+                                            counter is a slot of a per-device ring of 4096 allocated once
+                                            (cudaMalloc on first use) and zeroed on the launch's stream;
+                                            at most 4096 such launches may be in flight at once across
+                                            streams */
 
 /* The launch a gather of n rows would use (sorted != 0: dgz_gather_perm / the fetcher's sorted
  * path) with `cfg` (NULL = defaults): the resolved variant, SM count, warps per CTA, CTAs per SM,

@@ -292,7 +292,30 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
         }
         e = cudaHostRegister((void*)lo, hi - lo, rf);
         if (e == cudaErrorHostMemoryAlreadyRegistered) {
-            cudaGetLastError();  // pages already registered by someone else: map only
+            cudaGetLastError();
+            // pages already registered by someone else: map only -- if the WHOLE span is
+            // registered.  cudaHostRegister refuses a range that overlaps a registration at all,
+            // so a partial overlap would leave the rest unpinned and unmapped: probe the first
+            // and last byte and every 64 MiB between, and refuse the table otherwise.
+            bool covered = true;
+            const uintptr_t a0 = (uintptr_t)host_ptr, a1 = (uintptr_t)host_ptr + bytes - 1;
+            for (uintptr_t a = a0;; a += (uintptr_t(64) << 20)) {
+                const uintptr_t q = a < a1 ? a : a1;
+                void* dp = nullptr;
+                if (cudaHostGetDevicePointer(&dp, (void*)q, 0) != cudaSuccess) {
+                    cudaGetLastError();
+                    covered = false;
+                    break;
+                }
+                if (q == a1) break;
+            }
+            if (!covered) {
+                delete t;
+                set_error("dgz_register_table: [%p, +%zu) partly overlaps an existing host registration; "
+                          "register a span that shares no page with another registration",
+                          host_ptr, bytes);
+                return DGZ_ERR_STATE;
+            }
         } else if (e != cudaSuccess) {
             delete t;
             return cuda_fail(e, "cudaHostRegister");

@@ -21,6 +21,7 @@
 // element per thread (ablations for the fig:alignment_measurement analogue).  The shift
 // aligns to 128 BYTES (W = 128 / sizeof(T) elements; reading R3) with 64-bit offsets (R4).
 #include <atomic>
+#include <mutex>
 
 #include "internal.h"
 
@@ -462,6 +463,33 @@ static LaunchPlan plan_launch(const dgz_table_s* t, int64_t n, bool sorted_path,
     return LaunchPlan{variant, k, warps, cps, flags, blocked};
 }
 
+// Work counters of DGZ_GATHER_FLAG_DYNAMIC launches: a ring of kWorkCounters 8-byte slots per
+// device, allocated on first use and kept for the process.  Each launch takes the next slot and
+// zeroes it on its own stream, so launches on one stream are ordered, and launches on different
+// streams collide only if kWorkCounters of them are in flight at once.
+static constexpr int kWorkCounters = 4096;
+
+static unsigned long long* work_counter_slot(int dev) {
+    static std::mutex mu;
+    static unsigned long long* ring[64] = {};
+    static std::atomic<uint32_t> next[64];
+    if (dev < 0 || dev >= 64) { set_error("dgz_gather: device %d out of range", dev); return nullptr; }
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (!ring[dev]) {
+            unsigned long long* p = nullptr;
+            // allowed even while the caller's stream is being captured into a CUDA graph
+            cudaStreamCaptureMode m = cudaStreamCaptureModeRelaxed;
+            cudaThreadExchangeStreamCaptureMode(&m);
+            const cudaError_t e = cudaMalloc((void**)&p, sizeof(unsigned long long) * kWorkCounters);
+            cudaThreadExchangeStreamCaptureMode(&m);
+            if (e != cudaSuccess) { cuda_fail(e, "cudaMalloc (work counters)"); return nullptr; }
+            ring[dev] = p;
+        }
+    }
+    return ring[dev] + (next[dev].fetch_add(1, std::memory_order_relaxed) % kWorkCounters);
+}
+
 dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n, const int64_t* n_dev,
                            void* out, const dgz_gather_cfg* cfg, cudaStream_t s, const dgz_cache_view* cache) {
     DGZ_REQUIRE(t, "dgz_gather: null table");
@@ -477,7 +505,16 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
     }
     int dev = 0;
     DGZ_CUDA(cudaGetDevice(&dev));
-    if (dev != t->device && !(t->flags & (DGZ_REG_PORTABLE | DGZ_REG_VMM_BACKED))) {
+    if (dev != t->device && (t->flags & DGZ_REG_VMM_BACKED)) {
+        // VMM host memory is mapped only into the devices granted access: grant this one on
+        // demand (a no-op once granted) instead of letting the kernel touch an unmapped address
+        const int g = dgz_vmm_register(t->host, (size_t)t->rows * (size_t)t->row_bytes);
+        if (g != 1) {
+            if (g < 0) return (dgz_status)(-g);
+            set_error("dgz_gather: VMM table not accessible from device %d", dev);
+            return DGZ_ERR_STATE;
+        }
+    } else if (dev != t->device && !(t->flags & DGZ_REG_PORTABLE)) {
         set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
         return DGZ_ERR_STATE;
     }
@@ -511,20 +548,10 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
         const int sw = (int)(x & (~x + 1));
         unsigned long long* ctr = nullptr;
         if (flags & DGZ_GATHER_FLAG_DYNAMIC) {
-            // the 8-byte counter comes from the device's stream-ordered pool; keep the pool's memory
-            // reserved across synchronisations (release threshold) so that a fetch loop that syncs
-            // every step does not map fresh memory for each launch
-            static std::atomic<int> pool_tuned[64];
-            int devn = 0;
-            cudaGetDevice(&devn);
-            if (devn >= 0 && devn < 64 && !pool_tuned[devn].exchange(1)) {   // once per device, any thread
-                cudaMemPool_t pool;
-                if (cudaDeviceGetDefaultMemPool(&pool, devn) == cudaSuccess) {
-                    uint64_t thr = uint64_t(64) << 20;
-                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-                }
-            }
-            DGZ_CUDA(cudaMallocAsync((void**)&ctr, sizeof(unsigned long long), s));
+            // the work counter: one 8-byte slot of a per-device ring allocated once, zeroed in
+            // stream order before the launch (no allocation per launch, no pool attribute change)
+            ctr = work_counter_slot(dev);
+            if (!ctr) return DGZ_ERR_CUDA;
             DGZ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
         }
         SegLaunch L{cache ? &ca : nullptr, flags, dst_pos, n, n_dev, (uint8_t*)out, err, (int)blocks, warps * 32, blocked, s, ctr};
@@ -532,7 +559,6 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
             e = launch_segment_sw<int64_t>(sw, t, (const int64_t*)idx, L);
         else
             e = launch_segment_sw<int32_t>(sw, t, (const int32_t*)idx, L);
-        if (ctr) cudaFreeAsync(ctr, s);
     } else if (variant == DGZ_GATHER_NAIVE || variant == DGZ_GATHER_SHIFT) {
         int64_t blocks = (int64_t)k * 4;
         const bool sh = variant == DGZ_GATHER_SHIFT;

@@ -64,7 +64,10 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
     const uint64_t base = reinterpret_cast<uint64_t>(src);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    const int nconsumers = nwarps - 1;
+    // S is a multiple of nconsumers (launch_bulk): job j and job j + S (same slot) then run on the
+    // same consumer warp, so a consumer never waits on a slot's full barrier more than one phase
+    // ahead of it -- the parity wait of use u cannot be satisfied by phase u - 2 (ABA)
+    const int nconsumers = nwarps - 1 < S ? nwarps - 1 : S;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -118,7 +121,7 @@ gather_bulk_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t R, con
             }
             __syncwarp();
         }
-    } else {
+    } else if (warp - 1 < nconsumers) {
         using P = typename piece_t<SW>::T;
         for (int64_t j = warp - 1; j < njobs; j += nconsumers) {
             const int s = (int)(j % S);
@@ -148,6 +151,9 @@ cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, const int64_t* ds
     int S = (max_smem - 256) / (slot_bytes + 16);
     if (S > 1024) S = 1024;
     if (S < 2) return cudaErrorInvalidValue;
+    // consumers = min(warps - 1, S), and S rounded down to a multiple of them (see the kernel)
+    const int nc = threads / 32 - 1 < S ? threads / 32 - 1 : S;
+    S = S / nc * nc;
     const size_t smem = (((size_t)S * 16 + 127) & ~size_t(127)) + (size_t)S * slot_bytes;
     cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<SW, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -4,9 +4,12 @@
 // that mapping uses 4 KiB GPU pages (the mapping costs bytes/512 of HBM, exactly the paper's
 // 1/512), and random 512 B rows over a 57 GB table are then limited by address
 // translation, not by PCIe.  cuMemCreate with a HOST_NUMA location gives
-// pinned host memory that the driver maps into the GPU with large pages, still CPU-accessible
-// at the same virtual address, and exportable as a POSIX fd so that every per-GPU process can
-// map the same pages (the role Linux shm + per-process registration plays in P:616-627).
+// pinned host memory with a 2 MiB allocation granularity, CPU-accessible at the same virtual
+// address and exportable as a POSIX fd so that every per-GPU process can map the same pages
+// (the role Linux shm + per-process registration plays in P:616-627).  It was built to get
+// large GPU pages for sysmem; on the measured boxes the GPU still translated it at 4 KiB
+// (same 111 MB mapping cost, same random-row rate as cudaHostRegister: DESIGN.md section 5,
+// include/dgz.h DGZ_HOST_VMM), so it is an alternative allocator, not a faster one.
 #include <cuda.h>
 #include <unistd.h>
 

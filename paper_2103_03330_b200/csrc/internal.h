@@ -52,4 +52,7 @@ struct dgz_table_s {
 dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int64_t* dst_pos, int64_t n,
                            const int64_t* n_dev, void* out, const dgz_gather_cfg* cfg, cudaStream_t stream,
                            const dgz_cache_view* cache);
-int* dgz_table_flag(dgz_table t);  // flag for the current device (allocates on first use)
+int* dgz_table_flag(dgz_table t);
+// hostvmm.cu: 1 = inside a DGZ_HOST_VMM allocation (access granted to the current device), 0 = not,
+// negative = -dgz_status
+int dgz_vmm_register(const void* p, size_t bytes);  // flag for the current device (allocates on first use)

@@ -446,6 +446,28 @@ def order_ids(ids: torch.Tensor, max_id: int, stream=None) -> tuple:
     return srt, pos
 
 
+class Orderer:
+    """dgz_order_ids with outputs and workspace allocated once for lists of up to ``max_n`` IDs
+    (for loops that order a fresh list every step without allocating)."""
+
+    def __init__(self, max_n: int, device=None):
+        device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        v = _sz()
+        _check(_lib.dgz_order_workspace_bytes(max_n, ctypes.byref(v)), "dgz_order_workspace_bytes")
+        self.ws_bytes = v.value
+        self.ws = torch.empty(max(v.value, 1), dtype=torch.uint8, device=device)
+        self.srt = torch.empty(max(max_n, 1), dtype=torch.int64, device=device)
+        self.pos = torch.empty(max(max_n, 1), dtype=torch.int64, device=device)
+        self.max_n = max_n
+
+    def order(self, ids: torch.Tensor, max_id: int, n: int | None = None, stream=None) -> tuple:
+        n = ids.numel() if n is None else n
+        assert ids.dtype == torch.int64 and ids.is_cuda and n <= self.max_n
+        _check(_lib.dgz_order_ids(_dptr(ids), n, max_id, self.srt.data_ptr(), self.pos.data_ptr(), self.ws.data_ptr(),
+                                  self.ws_bytes, _stream(stream)), "dgz_order_ids")
+        return self.srt[:n], self.pos[:n]
+
+
 def check_errors(table: Table, stream=None) -> None:
     _check(_lib.dgz_check_errors(table.handle, _stream(stream)), "dgz_check_errors")
 

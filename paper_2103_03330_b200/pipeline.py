@@ -58,8 +58,12 @@ class MinibatchFetcher:
 
     def __init__(self, table: dgz.Table, graph: dgz.Graph, fanouts, max_seeds: int, slots: int = 2,
                  gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None,
-                 overlap_sampling: bool = False, sample_stream=None, sampler_sms: int | None = None, graphs: bool = False):
+                 overlap_sampling: bool = False, sample_stream=None, sampler_sms: int | None = None, graphs: bool = False,
+                 cache=None):
         self.table, self.graph = table, graph
+        # an HBM hot-row cache (dgz.HotRowCache / dgz.ShardedHotRowCache, NEXT-1): the gather reads
+        # cached rows from HBM (this GPU's or a peer's shard) and only the rest over PCIe
+        self.cache = cache
         # an HBM-resident table (dgz.DeviceTable) is gathered in frontier order (explore31)
         self.hbm_table = bool(table.info.flags & dgz.REG_DEVICE)
         if sampler_sms is None:
@@ -158,6 +162,9 @@ class MinibatchFetcher:
             if self.hbm_table:   # All-in-GPU: no address translation to save; write rows in order
                 dgz.gather(self.table, b.ids, self.rows[p], n=b.bounds[-1], n_dev=b.sizes_dev[L:L + 1],
                            cfg=self.cfg or dgz.gather_cfg(), stream=gs)
+            elif self.cache is not None:
+                self.cache.gather(b.ids_sorted, self.rows[p], dst_pos=b.ids_sorted_pos, n=b.bounds[-1],
+                                  n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=gs)
             else:
                 dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
                                 n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=gs)
@@ -176,6 +183,9 @@ class MinibatchFetcher:
         if self.hbm_table:
             dgz.gather(self.table, b.ids, self.rows[p], n=b.bounds[-1], n_dev=b.sizes_dev[L:L + 1],
                        cfg=self.cfg or dgz.gather_cfg(), stream=self.stream)
+        elif self.cache is not None:
+            self.cache.gather(b.ids_sorted, self.rows[p], dst_pos=b.ids_sorted_pos, n=b.bounds[-1],
+                              n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=self.stream)
         else:
             dgz.gather_perm(self.table, b.ids_sorted, b.ids_sorted_pos, self.rows[p], n=b.bounds[-1],
                             n_dev=b.sizes_dev[L:L + 1], cfg=self.cfg, stream=self.stream)

@@ -315,7 +315,11 @@ def test_step_sorted_gather_matches_oracle(dev, cid):
         t.close()
 
 
-@pytest.mark.parametrize("R,sms,warps,n", [(4096, 4, 8, 6000), (16384, 2, 4, 1500), (65536, 1, 4, 300), (512, 1, 2, 50000)])
+@pytest.mark.parametrize("R,sms,warps,n", [(4096, 4, 8, 6000), (16384, 2, 4, 1500), (65536, 1, 4, 300), (512, 1, 2, 50000),
+                                            # more consumer warps than ring slots, or S not a multiple of
+                                            # them (jobs j and j + S must share a consumer)
+                                            (40960, 2, 0, 700), (65536, 2, 0, 500), (8192, 2, 32, 4000),
+                                            (20000, 1, 8, 900), (30000, 3, 5, 800)])
 def test_bulk_ring_wraparound(dev, R, sms, warps, n):
     """BULK: many more rows per CTA than ring slots (slot reuse across many mbarrier phases),
     rows up to 64 KiB (ring of 3 slots), rows ending exactly at the end of the registered table."""
