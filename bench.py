@@ -43,6 +43,7 @@ import dgz_inputs as gen  # noqa: E402
 METRIC = "gathered feature GB/s per GPU and aggregate at 1/2/4/8 B200 vs PCIe Gen5 roofline"
 UNIT = "GB/s"
 SWEEP_BYTES = 256 << 20            # config 5: bytes of rows per step
+FORCE_MEMFD = os.environ.get("DGZ_BENCH_FORCE_MEMFD") == "1"   # tests: share host objects by memfd
 
 
 # ----------------------------------------------------------------------------------------------
@@ -186,13 +187,11 @@ def preflight(d: Dist, shared_bytes: int, per_rank_bytes: int) -> dict:
         if avail is not None and avail < need_ram:
             problems.append(f"host RAM: {avail / 1e9:.1f} GB available < {need_ram / 1e9:.1f} GB needed "
                             f"({shared_bytes / 1e9:.1f} GB table/CSR + {d.world} x {per_rank_bytes / 1e9:.1f} GB per rank)")
-        if d.world > 1:
+        if d.world > 1:   # a short /dev/shm is not fatal: the shared objects then live in memfds (shared_host_name)
             st = os.statvfs("/dev/shm")
             free = st.f_bavail * st.f_frsize
             info["dev_shm_free_gb"] = round(free / 1e9, 1)
-            if free < shared_bytes:
-                problems.append(f"/dev/shm: {free / 1e9:.1f} GB free < {shared_bytes / 1e9:.1f} GB for the shared table + CSR "
-                                "(remount with size=... or run fewer ranks)")
+            info["shared_objects"] = "/dev/shm" if free >= shared_bytes else "memfd of rank 0 (/dev/shm too small)"
     soft, _ = resource.getrlimit(resource.RLIMIT_MEMLOCK)
     lim_ok = soft == resource.RLIM_INFINITY or soft >= shared_bytes or os.geteuid() == 0
     info["memlock"] = "unlimited" if soft == resource.RLIM_INFINITY else soft
@@ -305,6 +304,22 @@ def workload_name(args) -> str:
 # ----------------------------------------------------------------------------------------------
 # shared inputs
 # ----------------------------------------------------------------------------------------------
+def shared_host_name(d: Dist, nbytes: int, tag: str):
+    """(name, fd to close after every rank mapped it) of a shared host object of `nbytes`: a /dev/shm
+    object when /dev/shm can hold it, else a memfd of rank 0 that the other ranks open through
+    /proc/<pid>/fd/<n> (shmem like /dev/shm, but not limited by the mount's size).  Collective."""
+    name, fd = None, None
+    if d.rank == 0:
+        st = os.statvfs("/dev/shm")
+        if st.f_bavail * st.f_frsize >= nbytes + (256 << 20) and not FORCE_MEMFD:
+            name = f"/dgz_bench_{tag}_{os.environ.get('MASTER_PORT', '0')}"
+        else:
+            fd = os.memfd_create(f"dgz_{tag}", 0)
+            os.ftruncate(fd, nbytes)
+            name = f"/proc/{os.getpid()}/fd/{fd}"
+    return d.bcast_obj(name), fd
+
+
 def make_table(cfg, d: Dist, dgz):
     """Host feature table: one copy on the box, registered by every rank."""
     nbytes = cfg.table_bytes
@@ -314,10 +329,10 @@ def make_table(cfg, d: Dist, dgz):
         gen.fill_table(buf.ptr, nbytes, cfg.seed)
         fill_s = time.time() - t0
     else:
-        name = f"/dgz_bench_c{cfg.cid}_{os.environ.get('MASTER_PORT', '0')}"
+        name, fd = shared_host_name(d, nbytes + 4096, f"c{cfg.cid}")
         fill_s = 0.0
         if d.rank == 0:   # interleaved over the sockets' memory when the box has several NUMA nodes
-            buf = dgz.HostBuffer(nbytes + 4096, shm_name=name, create=True,
+            buf = dgz.HostBuffer(nbytes + 4096, shm_name=name, create=fd is None,
                                  flags=dgz.HOST_HUGEPAGE | dgz.HOST_NUMA_INTERLEAVE)
             t0 = time.time()
             gen.set_threads(os.cpu_count() or 1)      # the other ranks are waiting: use every core
@@ -330,6 +345,8 @@ def make_table(cfg, d: Dist, dgz):
         d.barrier()
         if d.rank == 0:
             buf.unlink()   # the mappings stay valid; the name does not outlive the run
+            if fd is not None:
+                os.close(fd)
     return buf, fill_s
 
 
@@ -340,25 +357,36 @@ def make_csr(cfg, d: Dist, dgz, skew_alpha: float = 0.0):
     if d.world == 1:
         off, col = gen.gen_csr(cfg.n_nodes, cfg.avg_degree, cfg.seed, skew_alpha=skew_alpha)
         return off, col, int(off[-1]), []
-    base = f"/dgz_bench_csr{cfg.cid}_{os.environ.get('MASTER_PORT', '0')}"
-    bufs = []
+    bufs, names, fds = [], [], []
     e = None
     if d.rank == 0:
-        def alloc(nb):
-            b = dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{len(bufs)}", create=True, flags=dgz.HOST_NUMA_INTERLEAVE)
+        def alloc(nb):   # rank 0 only: a /dev/shm object, or a memfd when /dev/shm is short
+            st = os.statvfs("/dev/shm")
+            if st.f_bavail * st.f_frsize >= nb + (256 << 20) and not FORCE_MEMFD:
+                name, fd = f"/dgz_bench_csr{cfg.cid}_{os.environ.get('MASTER_PORT', '0')}_{len(bufs)}", None
+            else:
+                fd = os.memfd_create(f"dgz_csr{len(bufs)}", 0)
+                os.ftruncate(fd, nb + 4096)
+                name = f"/proc/{os.getpid()}/fd/{fd}"
+                fds.append(fd)
+            b = dgz.HostBuffer(nb + 4096, shm_name=name, create=fd is None, flags=dgz.HOST_NUMA_INTERLEAVE)
             bufs.append(b)
+            names.append(name)
             return b.ptr
         gen.set_threads(os.cpu_count() or 1)
         _, _, e = gen.gen_csr_into(cfg.n_nodes, cfg.avg_degree, cfg.seed, alloc, skew_alpha=skew_alpha)
         gen.set_threads(max(1, (os.cpu_count() or 1) // d.world))
-    e = int(d.bcast_obj(e))
+    e, names = d.bcast_obj((e, names))
+    e = int(e)
     if d.rank != 0:
-        for i, nb in enumerate(((cfg.n_nodes + 1) * 8, max(e * 4, 1))):
-            bufs.append(dgz.HostBuffer(nb + 4096, shm_name=f"{base}_{i}", create=False))
+        for name, nb in zip(names, ((cfg.n_nodes + 1) * 8, max(e * 4, 1))):
+            bufs.append(dgz.HostBuffer(nb + 4096, shm_name=name, create=False))
     d.barrier()
     if d.rank == 0:
         for b in bufs:
             b.unlink()
+        for fd in fds:
+            os.close(fd)
     off = bufs[0].numpy(0, (cfg.n_nodes + 1) * 8).view(np.int64)
     col = bufs[1].numpy(0, e * 4).view(np.int32)
     return off, col, e, bufs

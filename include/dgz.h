@@ -85,8 +85,12 @@ DGZ_API uint64_t dgz_kernel_launches(void);
 DGZ_API int dgz_host_numa_nodes(void);
 /* Map `bytes` of host memory.  shm_name == NULL: private anonymous mapping.  Otherwise a POSIX
  * shared-memory object (/dev/shm/<name>): create != 0 creates/truncates it to `bytes`,
- * create == 0 opens an existing object of at least `bytes` bytes.  *ptr receives a
- * page-aligned address.  The caller releases it with dgz_host_free. */
+ * create == 0 opens an existing object of at least `bytes` bytes.  A name containing a second '/'
+ * is a file path instead (a file on a tmpfs / hugetlbfs mount, or /proc/<pid>/fd/<n> naming
+ * another process's memfd), opened with open(2) -- for boxes whose /dev/shm is too small for the
+ * table; it must be shmem-backed for cudaHostRegister to pin it.  *ptr receives a page-aligned
+ * address.  The caller releases it with dgz_host_free.  dgz_host_unlink removes the name
+ * (shm_unlink / unlink; a no-op for /proc/<pid>/fd paths). */
 DGZ_API dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int create, uint32_t flags, void** ptr);
 DGZ_API dgz_status dgz_host_free(void* ptr, size_t bytes);
 DGZ_API dgz_status dgz_host_unlink(const char* shm_name);

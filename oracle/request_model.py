@@ -7,6 +7,9 @@ becomes one PCIe read request whose payload is the touched sectors (32/64/96/128
 - ``listing2_requests``: a literal transcription of Listing 2 with flat warp
   enumeration (warp = linear index // 32; SPEC S:240), with or without the circular shift
   stage.  Listing 2's line P:406-407 is garbled; reading R1 restores ``offset = i % feat_size``.
+  ``warp_size`` is Listing 2's alignment unit in ELEMENTS (32, literal); the repo's SHIFT ablation
+  aligns to 128 B (reading R3), i.e. ``warp_size = 128 // elem_size`` -- the same for 4-byte
+  elements, which is what the hardware comparisons use.
 - ``row_lines`` / ``row_sectors`` / ``segment_plan_requests``: the per-row minimum that the
   B200 kernel's 128 B-segment plan issues: every line a row touches is requested exactly once.
 """

@@ -147,8 +147,13 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
         }
     } else {
         DGZ_REQUIRE(shm_name[0] == '/', "dgz_host_alloc: shm name must start with '/'");
-        int fd = shm_open(shm_name, O_RDWR | (create ? O_CREAT : 0), 0600);
-        if (fd < 0) { set_error("shm_open(%s): %s", shm_name, strerror(errno)); return DGZ_ERR_NOMEM; }
+        // "/name": a POSIX shared-memory object (/dev/shm).  A name with a second '/' is a file
+        // path on a tmpfs / hugetlbfs (or /proc/<pid>/fd/<n> of another process's memfd): the
+        // fallback when /dev/shm is too small to hold the table
+        const bool path = strchr(shm_name + 1, '/') != nullptr;
+        int fd = path ? open(shm_name, O_RDWR | (create ? O_CREAT : 0), 0600)
+                      : shm_open(shm_name, O_RDWR | (create ? O_CREAT : 0), 0600);
+        if (fd < 0) { set_error("%s(%s): %s", path ? "open" : "shm_open", shm_name, strerror(errno)); return DGZ_ERR_NOMEM; }
         if (create) {
             if (ftruncate(fd, (off_t)bytes) != 0) {
                 set_error("ftruncate(%s, %zu): %s", shm_name, bytes, strerror(errno));
@@ -216,7 +221,9 @@ extern "C" dgz_status dgz_host_free(void* ptr, size_t bytes) {
 
 extern "C" dgz_status dgz_host_unlink(const char* shm_name) {
     DGZ_REQUIRE(shm_name, "dgz_host_unlink: null name");
-    if (shm_unlink(shm_name) != 0 && errno != ENOENT) {
+    if (strncmp(shm_name, "/proc/", 6) == 0) return DGZ_OK;   // a memfd: gone with its last reference
+    const int r = strchr(shm_name + 1, '/') ? unlink(shm_name) : shm_unlink(shm_name);
+    if (r != 0 && errno != ENOENT) {
         set_error("shm_unlink(%s): %s", shm_name, strerror(errno));
         return DGZ_ERR_INVALID;
     }

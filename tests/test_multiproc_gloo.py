@@ -20,10 +20,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, memfd=False):
     try:
         os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
-                           "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+                           "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port),
+                           "DGZ_BENCH_FORCE_MEMFD": "1" if memfd else "0"})
         sys.path.insert(0, ROOT)
         import bench
         import dgz_inputs as gen
@@ -57,11 +58,12 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(e)))
 
 
-def test_two_ranks_share_table_and_partition_batches():
+@pytest.mark.parametrize("memfd", [False, True])   # shared objects in /dev/shm, or rank 0's memfds (short /dev/shm)
+def test_two_ranks_share_table_and_partition_batches(memfd):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, memfd)) for r in range(2)]
     for p in ps:
         p.start()
     res = {}
