@@ -117,3 +117,16 @@ def test_chrome_trace(tmp_path):
     assert len(xs) == 3 and {e["tid"] for e in xs} == {1, 2, 3}
     g = [e for e in xs if e["name"] == "gather 0"][0]
     assert g["ts"] == 300.0 and abs(g["dur"] - 8700.0) < 1e-6
+
+
+def test_reference_arm_config5():
+    """The reference arm on a config-5 point (fp16 rows of an odd dim at a 4-byte base offset), on a
+    shrunken host buffer: the oracle gathers a bounded sample of the same lists our arm times."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "5",
+                        "--row-bytes", "66", "--dtype", "f16", "--base", "4", "--table-gb", "0.5", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][0])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["cores"] == 1
+    assert line["config"]["workload"] == bench.workload_name(_args(config=5, row_bytes=66, dtype="f16", base=4,
+                                                                    table_gb=0.5))
