@@ -1,0 +1,64 @@
+"""The small-row zero-copy gather is bound by GPU page walks, one per distinct 64 KiB region of the
+table, checked on the committed B200 records (profiles/r02/smallrow_study.jsonl,
+smallrow_ncu.csv; tools/smallrow_study.py, tools/smallrow_summary.py):
+
+- random sorted lists of 64-512 B rows: distinct 64 KiB regions translated per second is the same
+  (within 20 %) at every width, while rows/s differ 3x and GB/s 2.4x;
+- fixed-stride lists of 128 B rows: 4 KiB pages are not the unit (8 KiB strides run at 325 M pages/s),
+  the rate falls to the same ~64 M/s once every row is in its own 64 KiB region;
+- ncu: the traffic no SM issued (page walks) is 3.5-7 L2 sectors and ~150-210 B of DRAM reads per
+  distinct 64 KiB region -- one 128 B line of 16 PTEs plus upper levels, i.e. every region is walked
+  once (the sorted order leaves nothing to merge);
+- so rows/s = walk rate x rows per distinct region: the prediction for 128 B rows matches.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import smallrow_summary  # noqa: E402
+
+P = os.path.join(ROOT, "profiles", "r02")
+
+
+def _points():
+    timing = [json.loads(l) for l in open(os.path.join(P, "smallrow_study.jsonl"))]
+    return timing, smallrow_summary.ncu_launches(os.path.join(P, "smallrow_ncu.csv"))
+
+
+def test_walk_rate_is_constant_across_widths():
+    timing, _ = _points()
+    b = {t["R"]: t for t in timing if t["part"] == "B"}
+    rates = [b[R]["m_regions64k_s"] for R in (64, 128, 256, 512)]
+    mean = sum(rates) / len(rates)
+    assert (max(rates) - min(rates)) / mean < 0.2, rates
+    assert b[64]["mrows_s"] > 3 * b[512]["mrows_s"] and b[512]["gbs"] > 2.4 * b[64]["gbs"]
+    # rows/s predicted from the walk rate and the list's density (rows per distinct 64 KiB region)
+    pred = mean * b[128]["n"] / b[128]["regions64k"]
+    assert abs(pred - b[128]["mrows_s"]) / b[128]["mrows_s"] < 0.1, (pred, b[128]["mrows_s"])
+
+
+def test_unit_is_64k_not_4k():
+    timing, _ = _points()
+    a = {t["stride"]: t for t in timing if t["part"] == "A"}
+    assert a[128]["gbs"] > 45                                  # contiguous rows: the link
+    assert a[8192]["m_pages4k_s"] > 250                        # 4 KiB pages at > 250 M/s: not the limit
+    far = [a[s]["m_regions64k_s"] for s in (65536, 131072, 1 << 20)]
+    assert all(50 < r < 80 for r in far), far                  # one row per region: the walk rate
+    assert a[16384]["m_regions64k_s"] > 50 and a[16384]["mrows_s"] > 3 * a[65536]["mrows_s"]
+
+
+def test_walk_traffic_per_region():
+    timing, launches = _points()
+    for t, m in zip(timing, launches):
+        if t["part"] != "B" or t["R"] > 512:
+            continue
+        other = (m["lts__t_sectors.sum"] - m["lts__t_sectors_srcnode_gpc.sum"] - m["lts__t_sectors_srcunit_ltcfabric.sum"]
+                 - m["lts__t_sectors_srcunit_gcc.sum"])
+        per = other / t["regions64k"]
+        dram = m["dram__bytes_read.sum"] / t["regions64k"]
+        assert 3.5 < per < 7.0, (t["R"], per)
+        assert 120 < dram < 230, (t["R"], dram)
+        # the SMs' own traffic is the payload: sysmem sectors = rows x R / 32
+        assert m["syslts__t_sectors_srcunit_tex_aperture_sysmem_op_read_lookup_miss.sum"] == t["n"] * t["R"] // 32
