@@ -19,8 +19,35 @@ for R, base in ((512, 0), (2408, 8), (100, 4)):
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().reshape(-1, R), want), (R, v)
     o = np.argsort(idx, kind="stable")
-    dgz.gather_perm(t, torch.from_numpy(idx[o]).cuda(), torch.from_numpy(o.astype(np.int64)).cuda(), out)
-    torch.cuda.synchronize()
-    assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+    for cfg in (None, dgz.gather_cfg(sm_count=6, warps_per_cta=3, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)):
+        dgz.gather_perm(t, torch.from_numpy(idx[o]).cuda(), torch.from_numpy(o.astype(np.int64)).cuda(), out, cfg=cfg)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+    # the hot-row cache (two local shards) and the work-counter schedule through it
+    cache = dgz.HotRowCache(t, torch.from_numpy(idx[:300].copy()).cuda(), 2)
+    for cfg in (None, dgz.gather_cfg(flags=dgz.FLAG_DYNAMIC)):
+        cache.gather(torch.from_numpy(idx[o]).cuda(), out, dst_pos=torch.from_numpy(o.astype(np.int64)).cuda(), cfg=cfg)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+    del cache
     t.unregister(); buf.free()
-print("bulk/segment/naive/shift ok")
+# BULK with more consumer warps than ring slots (40 KiB rows, default warps)
+R, rows = 40960, 64
+buf = dgz.HostBuffer(rows * R + 8192)
+gen.fill_table(buf.ptr, rows * R, 3)
+t = dgz.register_table(buf.ptr, rows, R // 4, dgz.F32)
+idx = gen.random_ids(rows, 150, 2)
+want, _ = oracle.gather(buf.numpy(0, rows * R), R, idx)
+out = torch.empty(150 * R, dtype=torch.uint8, device="cuda")
+dgz.gather(t, torch.from_numpy(idx).cuda(), out, cfg=dgz.gather_cfg(variant=dgz.GATHER_BULK, sm_count=2))
+torch.cuda.synchronize()
+assert np.array_equal(out.cpu().numpy().reshape(-1, R), want)
+t.unregister(); buf.free()
+# the stand-in consumer
+x = torch.from_numpy(gen.float_table(2000 * 64, 1)).cuda()
+loc = torch.from_numpy(gen.random_ids(2000, 500 * 5, 4).astype(np.int32)).cuda()
+cnt = torch.full((500,), 5, dtype=torch.int32, device="cuda")
+y = torch.empty(500 * 64, dtype=torch.float32, device="cuda")
+dgz.aggregate_mean(x, 64, loc, cnt, 5, None, 500, y, repeat=2)
+torch.cuda.synchronize()
+print("bulk/segment/naive/shift/dynamic/cached/aggregate ok")
