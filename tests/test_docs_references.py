@@ -13,7 +13,7 @@ def _cited(path):
 
 def test_design_and_readme_citations_exist():
     missing = []
-    for doc in ("DESIGN.md", "README.md", "profiles/r01/README.md"):
+    for doc in ("DESIGN.md", "README.md", "profiles/r01/README.md", "profiles/r02/README.md", "tools/README.md"):
         for p in _cited(doc):
             full = os.path.join(ROOT, p)
             if not os.path.exists(full):
@@ -22,9 +22,10 @@ def test_design_and_readme_citations_exist():
 
 
 def test_profile_readme_lists_files():
-    listed = open(os.path.join(ROOT, "profiles", "r01", "README.md")).read()
-    for name in re.findall(r"`([\w.-]+\.(?:jsonl|json|csv|txt))`", listed):
-        if "*" in name:
-            continue
-        assert os.path.exists(os.path.join(ROOT, "profiles", "r01", name)) or \
-            os.path.exists(os.path.join(ROOT, "profiles", name)), name
+    for r in ("r01", "r02"):
+        listed = open(os.path.join(ROOT, "profiles", r, "README.md")).read()
+        for name in re.findall(r"`([\w.-]+\.(?:jsonl|json|csv|txt))`", listed):
+            if "*" in name:
+                continue
+            assert os.path.exists(os.path.join(ROOT, "profiles", r, name)) or \
+                os.path.exists(os.path.join(ROOT, "profiles", name)), name

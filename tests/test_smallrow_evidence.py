@@ -62,3 +62,28 @@ def test_walk_traffic_per_region():
         assert 120 < dram < 230, (t["R"], dram)
         # the SMs' own traffic is the payload: sysmem sectors = rows x R / 32
         assert m["syslts__t_sectors_srcunit_tex_aperture_sysmem_op_read_lookup_miss.sum"] == t["n"] * t["R"] // 32
+
+
+def test_walk_model_predicts_the_config4_gather():
+    """The headline kernel sits on the same walker bound: a config-4 minibatch (the bench's last
+    timed batches, recomputed here by the oracle) touches ~0.53 M distinct 64 KiB regions of the
+    56.9 GB table; at the walk rate measured on random lists that is the measured gather time."""
+    import numpy as np
+    import dgz_inputs as gen
+    import oracle
+    line = json.load(open(os.path.join(P, "bench_config4.json")))
+    c = gen.CONFIGS[4]
+    off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+    regions = []
+    for b in line["parity"]["batches"]:
+        j = b["j"]
+        s = oracle.sample_uniform(off, col, gen.batch_seeds(c.n_nodes, c.batch, c.seed, j), c.fanouts,
+                                  gen.batch_rng_seed(c.seed, j), with_blocks=False)
+        assert s.U.shape[0] == b["rows"]
+        regions.append(np.unique((s.U * c.row_bytes) >> 16).shape[0])
+    timing, _ = _points()
+    rate = sum(t["m_regions64k_s"] for t in timing if t["part"] == "B" and t["R"] <= 512) / 4 * 1e6
+    t_walk_ms = float(np.mean(regions)) / rate * 1e3
+    t_meas = line["roofline"]["gather_ms_mean"]
+    assert 0.5e6 < np.mean(regions) < 0.56e6
+    assert abs(t_walk_ms - t_meas) / t_meas < 0.08, (t_walk_ms, t_meas)
