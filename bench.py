@@ -438,14 +438,51 @@ def measure_ceilings(dgz, d: Dist):
     el = a.elapsed_time(b) * 1e-3
     zc = 4 * zbytes / el / 1e9
     zc_agg = d.allreduce([4.0 * zbytes], "sum")[0] / d.allreduce([el], "max")[0] / 1e9
+    rtt = measure_rtt(dgz, pbuf, ptab)
     ptab.unregister()
     pbuf.free()
     del dbuf
     return {"h2d_dma_gbs": round(dma, 2), "h2d_dma_trials": [round(x, 2) for x in trials], "zc_stream_gbs": round(zc, 2),
             "ranks": d.world, "h2d_dma_aggregate_gbs": round(max(agg), 2), "zc_stream_aggregate_gbs": round(zc_agg, 2),
+            "rtt": rtt,
             "how": "every rank at once after a barrier: best of 8 x (cudaMemcpyAsync 256 MiB pinned H2D x10) after 40 "
                    "warm-up copies; zero-copy "
                    "LDG.128 stream over a 1 GiB pinned buffer x4 on 8 SMs; aggregate = sum bytes / max time over ranks"}
+
+
+def measure_rtt(dgz, pbuf, ptab, hops: int = 1000):
+    """Round trip of one dependent zero-copy load (the Little's-law input): a pointer chase
+    by one thread through the pinned buffer, (a) over 128 B lines inside 64 KiB regions already
+    translated (the PCIe round trip), (b) one hop per fresh 64 KiB region (round trip + page walk).
+    Cycles per hop at the SM clock; ns at the max SM clock of MEASURED_PEAKS.json."""
+    arr = pbuf.numpy().view(np.int64)
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    out = {}
+    rng = np.random.default_rng(7)
+    cyc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for name, stride, base, m in (("in_region", 128, 0, 512), ("new_region", 65536, 64 << 20, hops)):
+        slots = base // 8 + np.arange(m, dtype=np.int64) * (stride // 8)   # m nodes of one cycle
+        order = rng.permutation(m)
+        if name == "in_region":
+            order = np.concatenate([[0], order[order != 0]])   # the chase starts at element 0
+        for k in range(m):     # values are element indices from the buffer start (the chase's p)
+            arr[slots[order[k]]] = slots[order[(k + 1) % m]]
+        if name == "new_region":
+            arr[0] = slots[order[0]]                             # element 0 -> the first fresh region
+        if name == "in_region":     # one 64 KiB region: translate it once, then time the round trips
+            dgz.probe_chase(ptab.info.dev_ptr, m, cyc)
+        torch.cuda.synchronize()
+        dgz.probe_chase(ptab.info.dev_ptr, hops, cyc)
+        torch.cuda.synchronize()
+        c = cyc[0].item() / hops
+        out[name] = {"cycles": round(c, 1), "us_at_max_clock": round(c / mhz, 3)}
+    out["how"] = "dgz_probe_chase: one thread, dependent ld.global.cv over the pinned buffer, 1000 hops"
+    return out
 
 
 def hbm_peak() -> float:
@@ -614,6 +651,9 @@ def run_ours(args, d: Dist):
         dma_base = run_dma_baseline(cfg, buf, fetcher, seeds_dev, rng, K, d, cpus, node)
         if rank == 0:
             cpu_base, parity = run_oracle_leg(cfg, buf.ptr, off, col, last, d, cpus[0], budget=args.oracle_budget)
+    all_in_gpu = None
+    if G == 1 and not args.no_baselines and args.csr == "hbm" and cache is None:
+        all_in_gpu = run_all_in_gpu(dgz, cfg, buf, graph, seeds_dev, rng, K)
     d.barrier()
 
     clocks = clk.summary()
@@ -671,6 +711,7 @@ def run_ours(args, d: Dist):
                                              "sample start -> gather end spans about two gathers"}},
         "rows_per_step_mean": round(float(np.mean(ns)), 1),
         "cpu_baseline": cpu_base, "dma_baseline": dma_base, "parity": parity, "cache_stats": cache_stats,
+        "all_in_gpu": all_in_gpu,
         "e2e": e2e, "overlap": overlap, "per_rank": per_rank,
         "gpu_launches": int(launches), "gpu_launches_per_step": round(launches / K, 2),
         "clocks": clocks,
@@ -1002,6 +1043,43 @@ def run_oracle_leg(cfg, table_addr, off, col, last, d: Dist, core: int, budget: 
              "s_per_minibatch": round(t_total / nb, 3), "host_cores": os.cpu_count(), "core": core,
              "ranks": d.world, "note": "rank 0 only, after the timed region, pinned to one core of its GPU's NUMA node"},
             parity)
+
+
+def run_all_in_gpu(dgz, cfg, buf, graph, seeds_dev, rng, K):
+    """Context only (the paper's All-in-GPU): the whole table copied
+    into HBM once and fetched by the same sampler + gather kernels (frontier order, HBM-speed gather);
+    the bound any host-memory method is compared against.  N = 1 only (one 56.9 GB HBM copy)."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+    R = cfg.row_bytes
+    dev = torch.empty(cfg.table_bytes, dtype=torch.uint8, device="cuda")
+    dev.copy_(torch.from_numpy(buf.numpy(0, cfg.table_bytes)))      # registered pages: one DMA
+    dtab = dgz.DeviceTable(dev.data_ptr(), cfg.n_nodes, cfg.dim, dgz.F32)
+    f = MinibatchFetcher(dtab, graph, cfg.fanouts, cfg.batch, sampler_sms=0)
+    nb = min(K, 8)
+    for i in range(2):
+        f.fetch(seeds_dev[i], rng[i])
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    mbs = []
+    cnt = torch.zeros(nb, dtype=torch.int64, device="cuda")
+    a.record(f.stream)
+    for i in range(nb):
+        mbs.append(f.fetch(seeds_dev[i], rng[i], timing=True, count_into=cnt[i:i + 1]))
+    b.record(f.stream)
+    torch.cuda.synchronize()
+    g_ms = [mb.timing[1].elapsed_time(mb.timing[2]) for mb in mbs]
+    el = a.elapsed_time(b) * 1e-3
+    n_mean = float(cnt.double().mean())
+    out = {"step_gbs": round(n_mean * R * nb / el / 1e9, 1), "gather_gbs": round(n_mean * R / (float(np.mean(g_ms)) * 1e-3) / 1e9, 1),
+           "ms_per_step": round(el / nb * 1e3, 3), "gather_ms": round(float(np.mean(g_ms)), 3),
+           "hbm_traffic_frac": round(2 * n_mean * R / (float(np.mean(g_ms)) * 1e-3) / 1e9 / hbm_peak(), 3),
+           "how": "table copied to HBM (dgz_wrap_device_table), same fetcher, sample then gather on one stream, "
+                  f"{nb} minibatches (GB/s of useful bytes; HBM traffic = reads + writes of the rows)"}
+    f.close()
+    dtab.unregister()
+    del dev
+    torch.cuda.empty_cache()
+    return out
 
 
 def _chunked_dma(host_rows, ids_cpu, R, stage, dst, cs, done):
