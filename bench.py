@@ -1165,7 +1165,8 @@ def run_rowsweep(args, d: Dist):
     total = c4.table_bytes
     rows = (total - base) // R
     n = min(rows, SWEEP_BYTES // R)
-    pre = preflight(d, total, 2 * (32 << 20) + (3 << 30) + n * 8 * 2)
+    # per rank: the ID lists on the host and their pinned copies (e2e leg), DMA staging, ceilings' buffers
+    pre = preflight(d, total, 2 * (W + K) * n * 8 + 2 * (32 << 20) + (3 << 30))
     t_setup = time.time()
     gen.set_threads(max(1, (os.cpu_count() or 1) // G))
     buf, fill_s = make_table(c4, d, dgz)
