@@ -924,7 +924,6 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
     cands = OVERLAP_CANDIDATES
     if args.overlap_warps:
         cands = tuple((k, sp, args.overlap_warps) for k, sp, _ in cands)
-    best_shape = None
     for k, spread, w in cands:
         try:
             part = dgz.Partition(k, -1, dgz.PARTITION_SPREAD if spread else 0)
@@ -937,19 +936,23 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
         # flight win
         pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=w, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
         # sampler placement: in front of the gather on the small partition, or in the consumer's stream
-        # between consumer steps -- both measured
-        for where in ("fetch partition", "consumer stream"):
+        # between consumer steps; consumer on the complementary partition, or on the whole GPU (a plain
+        # stream: its CTAs then also fill the fetch partition's SMs) -- all measured
+        for where, cons in (("fetch partition", "partition"), ("consumer stream", "partition"),
+                            ("fetch partition", "whole GPU")):
+            comp = part.compute_stream if cons == "partition" else comp0
             f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream,
-                                 gather_cfg=pcfg, sample_stream=part.compute_stream if where == "consumer stream" else None)
-            t_g, t_c, t_o, _, _, t_of = measure(f, part.compute_stream, repeat=repeat)
-            rows.append({"partition": f"green context ({shape}), sampler in the {where}", "fetch_sms": part.fetch_sms,
-                         "warps_per_sm": w, "compute_sms": part.compute_sms,
+                                 gather_cfg=pcfg, sample_stream=comp if where == "consumer stream" else None)
+            t_g, t_c, t_o, _, _, t_of = measure(f, comp, repeat=repeat)
+            rows.append({"partition": f"green context ({shape}), sampler in the {where}, consumer on the "
+                                      + ("other SMs" if cons == "partition" else "whole GPU"),
+                         "fetch_sms": part.fetch_sms, "warps_per_sm": w,
+                         "compute_sms": part.compute_sms if cons == "partition" else 148,
                          "t_fetch_ms": round(t_g, 3), "t_consumer_ms": round(t_c, 3), "t_step_overlapped_ms": round(t_o, 3),
                          "t_step_overlapped_incl_fill_ms": round(t_of, 3),
                          "exposed_fetch_ms": round(max(0.0, t_o - t_c), 3),
-                         "fetch_gbs_alone": round(float(f.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2)})
-            if best_shape is None or t_o < best_shape[0]:
-                best_shape = (t_o, k, spread, w, where)
+                         "fetch_gbs_alone": round(float(f.bufs[0].sizes_host[-1]) * cfg.row_bytes / t_g / 1e6, 2),
+                         "shape": [k, spread, w, where, cons]})
             del f
         torch.cuda.synchronize()
         part.destroy()
@@ -959,17 +962,18 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
     t_best = min(r["t_step_overlapped_ms"] for r in cand)
     best = min((r for r in cand if r["t_step_overlapped_ms"] <= 1.01 * t_best), key=lambda r: r["exposed_fetch_ms"])
     timeline = None
-    if best_shape is not None:   # the best shape again, with per-step events on every stream
-        _, k, spread, w, where = best_shape
+    if "shape" in best:   # the best shape again, with per-step events on every stream
+        k, spread, w, where, cons = best["shape"]
         part = dgz.Partition(k, -1, dgz.PARTITION_SPREAD if spread else 0)
+        comp = part.compute_stream if cons == "partition" else comp0
         pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=w, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
         f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=part.fetch_stream,
-                             gather_cfg=pcfg, sample_stream=part.compute_stream if where == "consumer stream" else None)
-        t_g, t_c, t_o, _, tl, _ = measure(f, part.compute_stream, repeat=repeat, timeline=True)
+                             gather_cfg=pcfg, sample_stream=comp if where == "consumer stream" else None)
+        t_g, t_c, t_o, _, tl, _ = measure(f, comp, repeat=repeat, timeline=True)
         del f
         torch.cuda.synchronize()
         part.destroy()
-        timeline = {"shape": {"fetch_sms": k, "spread": spread, "warps_per_sm": w, "sampler": where},
+        timeline = {"shape": {"fetch_sms": k, "spread": spread, "warps_per_sm": w, "sampler": where, "consumer": cons},
                     "t_step_overlapped_ms": round(t_o, 3), "steps": tl,
                     "how": "CUDA events around each phase on its own stream, ms from the first consumer step's start"}
         if args.timeline:
