@@ -10,7 +10,10 @@ memory.  Strategies compared on the same minibatches (GPU sampler, same model, s
           rows into pinned staging (torch.index_select), cudaMemcpyAsync H2D; double-buffered so the
           CPU gather of j+1 overlaps the training of j;
   hbm  -- "All-in-GPU": the whole table copied into HBM once (56.9 GB fits B200's
-          180 GB) and gathered by the same kernel at HBM speed -- the lower bound on step time.
+          180 GB) and gathered by the same kernel at HBM speed -- the lower bound on step time;
+  uvm / uvm_host -- the UVM strategy: the table in CUDA managed memory, migrated into HBM
+          on GPU page faults (uvm; the first pass is the cold cost) or kept in host memory and read
+          through the GPU's mapping (uvm_host: preferred location CPU, accessed by the GPU).
 
 The model is plain PyTorch (mean-aggregator SAGE layers): it is not the hot path, the
 fetch is.  The table holds random bytes, not meaningful features: inputs are clamped to finite
@@ -109,7 +112,7 @@ def dump_minibatch(path, j, ids, rows, blocks=None):
 
 
 def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sample_on="compute", spread=False,
-                     tune=False, fetch_warps=8, dump=None):
+                     tune=False, fetch_warps=8, dump=None, order=None, cold=False):
     """zc / hbm: gather on a `fetch_sms` green-context partition, training on the others.  The
     sampler (HBM-bound, ~0.3 ms on the big partition) runs either in the training stream between
     steps (`compute`) or in front of the gather on the fetch partition (`fetch`)."""
@@ -131,7 +134,7 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
         pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=fetch_warps, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
     comp = part.compute_stream
     f = MinibatchFetcher(table, graph, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=pcfg,
-                         sample_stream=comp if sample_on == "compute" else None)
+                         sample_stream=comp if sample_on == "compute" else None, order=order)
     with torch.cuda.stream(comp):   # model (and DDP's buckets) created on the stream that trains
         trainer = make_trainer()
     torch.cuda.synchronize()
@@ -139,6 +142,7 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
     def fetch_alone():
         for i in range(K):
             f.fetch(seeds[i], rng[i]).sizes()
+    t_first = timed(fetch_alone, K)[0] if cold else None   # the first pass over a cold table (UVM: page faults)
     for i in range(2):
         fetch_alone()
     t_fetch, _ = timed(fetch_alone, K)
@@ -174,10 +178,36 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
            "fetch_partition": ("tuned: " + json.dumps(tuned)) if tuned else ("spread over the GPCs" if spread else "contiguous"),
            "fetch_warps_per_sm": pcfg.warps_per_cta,
            "rows_per_minibatch": sz[-1]}
+    if t_first is not None:
+        out["first_pass_fetch_ms"] = round(t_first, 3)
     f.close()
     torch.cuda.synchronize()
     part.destroy()
     return out
+
+
+def managed_table(c, buf, host_preferred):
+    """The UVM strategy: the table in CUDA managed memory, filled by the CPU (so it starts
+    resident in host memory).  host_preferred=False: the default policy -- GPU accesses fault and the
+    driver migrates pages into HBM (B200's HBM holds the whole table, so later passes run from HBM);
+    True: cudaMemAdviseSetPreferredLocation(CPU) + SetAccessedBy(GPU) -- pages stay in host memory and
+    the GPU reads them through its mapping (UVM's own zero-copy).  Returns (pointer, free())."""
+    import ctypes
+    from cuda.bindings import runtime as rt
+    err, ptr = rt.cudaMallocManaged(c.table_bytes, rt.cudaMemAttachGlobal)
+    assert err == rt.cudaError_t.cudaSuccess, err
+    dst = np.ctypeslib.as_array((ctypes.c_uint8 * c.table_bytes).from_address(int(ptr)))
+    src = buf.numpy(0, c.table_bytes)
+    step = 1 << 30
+    for o in range(0, c.table_bytes, step):
+        dst[o:o + step] = src[o:o + step]
+    if host_preferred:
+        dev = torch.cuda.current_device()
+        for adv, where in ((rt.cudaMemoryAdvise.cudaMemAdviseSetPreferredLocation, rt.cudaCpuDeviceId),
+                           (rt.cudaMemoryAdvise.cudaMemAdviseSetAccessedBy, dev)):
+            (e,) = rt.cudaMemAdvise(ptr, c.table_bytes, adv, where)
+            assert e == rt.cudaError_t.cudaSuccess, e
+    return int(ptr), (lambda: rt.cudaFree(ptr))
 
 
 def run_dma_mode(host_rows, graph, c, seeds, rng, K, threads, trainer, dump=None):
@@ -301,7 +331,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--hidden", type=int, default=256)
     ap.add_argument("--classes", type=int, default=172)      # ogbn-papers100M has 172 classes
-    ap.add_argument("--modes", default="zc,dma,hbm")
+    ap.add_argument("--modes", default="zc,dma,hbm", help="any of zc, dma, hbm, uvm, uvm_host")
     ap.add_argument("--fetch-sms", type=int, default=32)
     ap.add_argument("--sample-on", default="compute", choices=["compute", "fetch"])
     ap.add_argument("--contiguous", dest="spread", action="store_false",
@@ -373,16 +403,29 @@ def main():
                                      a.fetch_warps)
         dtab.unregister()
         del dev
+    for m in ("uvm", "uvm_host"):   # the paper's UVM strategy, both placements (same fetcher, address order)
+        if m in modes:
+            ptr, free = managed_table(c, buf, host_preferred=(m == "uvm_host"))
+            utab = dgz.DeviceTable(ptr, c.n_nodes, c.dim, dgz.F32)
+            res[m] = run_fetcher_mode(utab, graph, c, seeds, rng, K, a.fetch_sms,
+                                      lambda: Trainer(c, a.hidden, a.classes, G > 1), a.sample_on, a.spread, a.tune,
+                                      a.fetch_warps, order="sorted", cold=True)
+            utab.unregister()
+            torch.cuda.synchronize()
+            free()
     if G > 1:   # per-rank results to rank 0; the job's step time is the slowest rank's
         allres = [None] * G
-        dist.all_gather_object(allres, {m: res[m] for m in ("zc", "dma", "hbm") if m in res})
-        for m in ("zc", "dma", "hbm"):
+        dist.all_gather_object(allres, {m: res[m] for m in ("zc", "dma", "hbm", "uvm", "uvm_host") if m in res})
+        for m in ("zc", "dma", "hbm", "uvm", "uvm_host"):
             if m in res:
                 res[m] = {"step_ms": max(r[m]["step_ms"] for r in allres), "per_rank": [r[m] for r in allres]}
     if "zc" in res and "dma" in res:
         res["speedup_zc_over_dma"] = round(res["dma"]["step_ms"] / res["zc"]["step_ms"], 3)
     if "zc" in res and "hbm" in res:
         res["zc_vs_all_in_gpu"] = round(res["hbm"]["step_ms"] / res["zc"]["step_ms"], 3)
+    for m in ("uvm", "uvm_host"):
+        if "zc" in res and m in res:
+            res[f"speedup_zc_over_{m}"] = round(res[m]["step_ms"] / res["zc"]["step_ms"], 3)
     if rank == 0:
         print(json.dumps(res), flush=True)
     table.unregister()

@@ -59,13 +59,16 @@ class MinibatchFetcher:
     def __init__(self, table: dgz.Table, graph: dgz.Graph, fanouts, max_seeds: int, slots: int = 2,
                  gather_cfg: dgz.GatherCfg | None = None, blocks: bool = True, fetch_stream=None,
                  overlap_sampling: bool = False, sample_stream=None, sampler_sms: int | None = None, graphs: bool = False,
-                 cache=None):
+                 cache=None, order: str | None = None):
         self.table, self.graph = table, graph
         # an HBM hot-row cache (dgz.HotRowCache / dgz.ShardedHotRowCache, NEXT-1): the gather reads
         # cached rows from HBM (this GPU's or a peer's shard) and only the rest over PCIe
         self.cache = cache
         # an HBM-resident table (dgz.DeviceTable) is gathered in frontier order (explore31)
         self.hbm_table = bool(table.info.flags & dgz.REG_DEVICE)
+        if order is not None:      # "sorted" (address order) / "frontier": override the table-kind default
+            assert order in ("sorted", "frontier")
+            self.hbm_table = order == "frontier"
         if sampler_sms is None:
             # A zero-copy CSR (dgz.HostGraph) makes the sampler a stream of small PCIe reads: beside
             # the gather both slow down (36 vs 37.8 GB/s sequential, config 4), so it runs back to

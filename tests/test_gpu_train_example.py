@@ -83,3 +83,16 @@ def test_train_example_ddp_two_ranks(tmp_path):
         _oracle_anchor(tmp_path / f"zc_rank{rank}.npz", True)
         _oracle_anchor(tmp_path / f"dma_rank{rank}.npz", False)
     assert int(np.load(tmp_path / "zc_rank1.npz")["j"]) == 1
+
+
+def test_train_example_uvm_modes():
+    """The UVM baselines (managed memory: migrated on fault / host-preferred and mapped) train on the
+    same minibatches through the same fetcher; the losses equal the zero-copy run's (same rows)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, EX, "--config", "1", "--steps", "3", "--fetch-sms", "8", "--modes", "zc,uvm,uvm_host"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _check(r.stdout, ("zc", "uvm", "uvm_host"))
+    for m in ("uvm", "uvm_host"):
+        assert d[m]["first_pass_fetch_ms"] > 0 and d[m]["loss"] == d["zc"]["loss"]
