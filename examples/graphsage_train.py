@@ -131,7 +131,8 @@ def run_fetcher_mode(table, graph, c, seeds, rng, K, fetch_sms, make_trainer, sa
         del probe
     else:
         part = dgz.Partition(fetch_sms, -1, dgz.PARTITION_SPREAD if spread else 0)
-        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=fetch_warps, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
+        pcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=fetch_warps,
+                              flags=dgz.FLAG_DEEP | (0 if os.environ.get("DGZ_TRAIN_STATIC") == "1" else dgz.FLAG_DYNAMIC))
     comp = part.compute_stream
     f = MinibatchFetcher(table, graph, c.fanouts, c.batch, fetch_stream=part.fetch_stream, gather_cfg=pcfg,
                          sample_stream=comp if sample_on == "compute" else None, order=order)
