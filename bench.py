@@ -320,9 +320,36 @@ def shared_host_name(d: Dist, nbytes: int, tag: str):
     return d.bcast_obj(name), fd
 
 
-def make_table(cfg, d: Dist, dgz):
-    """Host feature table: one copy on the box, registered by every rank."""
+HOST_TABLE_POLICY = {
+    "managed": "DGZ_HOST_MANAGED: cudaMallocManaged, preferred location CPU (filled in place by the CPU, never "
+               "migrates), AccessedBy the GPU at registration; one copy per rank",
+    "registered": "/dev/shm object shared by the ranks (NUMA-interleaved), cudaHostRegister'd by every rank"}
+
+
+def host_table_kind(args, d: Dist, nbytes: int) -> str:
+    """'managed' (DGZ_HOST_MANAGED: CUDA managed memory kept in host memory, mapped for the GPU with
+    large pages -- DESIGN.md 5.1) or 'registered' (the paper's cudaHostRegister'd table, one shared
+    /dev/shm copy per box).  auto: managed when every rank can hold its own copy in host
+    RAM (managed memory is not shareable across processes), else registered.  Collective."""
+    kind = args.host_table
+    if kind == "auto":
+        kind = "managed"
+        if d.world > 1:
+            avail = _meminfo_bytes("MemAvailable") or 0
+            kind = "managed" if d.world * nbytes <= 0.7 * avail else "registered"
+            kind = d.bcast_obj(kind)
+    return kind
+
+
+def make_table(cfg, d: Dist, dgz, kind: str = "registered"):
+    """Host feature table.  registered: one copy on the box, registered by every rank (P:616-627);
+    managed: one DGZ_HOST_MANAGED copy per rank, filled in place by the CPU."""
     nbytes = cfg.table_bytes
+    if kind == "managed":
+        buf = dgz.HostBuffer(nbytes + 4096, flags=dgz.HOST_MANAGED)
+        t0 = time.time()
+        gen.fill_table(buf.ptr, nbytes, cfg.seed)
+        return buf, time.time() - t0
     if d.world == 1:
         buf = dgz.HostBuffer(nbytes + 4096, flags=dgz.HOST_HUGEPAGE)
         t0 = time.time()
@@ -533,10 +560,13 @@ def run_ours(args, d: Dist):
     G, rank = d.world, d.rank
     csr_bytes = (cfg.n_nodes + 1) * 8 + int(cfg.n_nodes * cfg.avg_degree * 1.01) * 4
     bound = gen.sample_bound(cfg.n_nodes, cfg.batch, cfg.fanouts)[-1]
-    pre = preflight(d, cfg.table_bytes + csr_bytes, 2 * bound * R + (3 << 30) + (csr_bytes if G == 1 else 0))
+    tkind = host_table_kind(args, d, cfg.table_bytes)
+    per_rank_tab = cfg.table_bytes if tkind == "managed" else 0
+    pre = preflight(d, (cfg.table_bytes if tkind == "registered" else 0) + csr_bytes,
+                    2 * bound * R + (3 << 30) + (csr_bytes if G == 1 else 0) + per_rank_tab)
     t_setup = time.time()
     gen.set_threads(max(1, (os.cpu_count() or 1) // G))
-    buf, fill_s = make_table(cfg, d, dgz)
+    buf, fill_s = make_table(cfg, d, dgz, tkind)
     d.barrier()
     table = dgz.register_table(buf.ptr, cfg.n_nodes, cfg.dim, dgz.F32)
     info = table.info
@@ -682,6 +712,7 @@ def run_ours(args, d: Dist):
                    "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
                    "pipeline": fetcher.mode, "pipeline_choice": choice,
                    "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else "pinned host memory, sampled by zero-copy",
+                   "host_table": tkind,
                    "gather": dict(dgz.gather_plan(table, cap, True, gcfg),
                                   order="address-sorted + inverse permutation (dgz_gather_perm)"),
                    "cache": cache_info},
@@ -720,8 +751,8 @@ def run_ours(args, d: Dist):
                   "mapping_ratio": round(cfg.table_bytes / max(info.gpu_mem_delta, 1), 1),
                   "csr_gen_s": round(csr_s, 2), "total_s": round(time.time() - t_setup, 1), "sms": sm_count,
                   "host_numa_nodes": dgz.host_numa_nodes(), "preflight": pre,
-                  "host_table_policy": "anonymous THP mapping (first touch)" if G == 1 else
-                                       "/dev/shm object shared by the ranks, NUMA-interleaved"},
+                  "host_table_policy": HOST_TABLE_POLICY[tkind] if tkind == "managed" or G > 1 else
+                                       "anonymous THP mapping (first touch), cudaHostRegister"},
     }
     fetcher.close()
     if cache is not None and G > 1:
@@ -1204,10 +1235,12 @@ def run_rowsweep(args, d: Dist):
     rows = (total - base) // R
     n = min(rows, SWEEP_BYTES // R)
     # per rank: the ID lists on the host and their pinned copies (e2e leg), DMA staging, ceilings' buffers
-    pre = preflight(d, total, 2 * (W + K) * n * 8 + 2 * (32 << 20) + (3 << 30))
+    tkind = host_table_kind(args, d, total)
+    pre = preflight(d, total if tkind == "registered" else 0,
+                    2 * (W + K) * n * 8 + 2 * (32 << 20) + (3 << 30) + (total if tkind == "managed" else 0))
     t_setup = time.time()
     gen.set_threads(max(1, (os.cpu_count() or 1) // G))
-    buf, fill_s = make_table(c4, d, dgz)
+    buf, fill_s = make_table(c4, d, dgz, tkind)
     d.barrier()
     table = dgz.register_table(buf.ptr + base, rows, R // eb, dtype)
     info = table.info
@@ -1322,7 +1355,7 @@ def run_rowsweep(args, d: Dist):
         "ms_per_step": round(max_el / K * 1e3, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": f"u8 ({args.dtype} rows moved as bytes)", "data": "synthetic",
         "config": {"workload": workload_name(args), "row_bytes": R, "base_offset": base, "elem": args.dtype, "rows": rows,
-                   "rows_per_step": n, "parallelism": f"dp{G} (independent ID lists per rank)",
+                   "rows_per_step": n, "parallelism": f"dp{G} (independent ID lists per rank)", "host_table": tkind,
                    "l2": "inputs larger than L2 (56.9 GB table, a fresh 256 MiB ID list every step)",
                    "gather": dict(dgz.gather_plan(table, n, True, None), order="dgz_order_ids + dgz_gather_perm")},
         "per_gpu_gbs": round(per_gpu, 3),
@@ -1470,6 +1503,9 @@ def main():
                     help="configs 1-4: cache this fraction of the rows (highest in-degree) in HBM, sharded over the ranks "
                          "(NEXT-1), on the power-law variant of the graph")
     ap.add_argument("--skew-alpha", type=float, default=3.0, help="power-law exponent of the graph with --cache-frac")
+    ap.add_argument("--host-table", default="auto", choices=["auto", "managed", "registered"],
+                    help="feature table in managed host memory (large GPU pages) or cudaHostRegister'd (the paper's "
+                         "unified tensor, one shared copy per box); auto: managed when every rank can hold a copy")
     ap.add_argument("--gather-sms", type=int, default=0)
     ap.add_argument("--gather-warps", type=int, default=0)
     ap.add_argument("--sampler-sms", type=int, default=None,

@@ -81,6 +81,16 @@ DGZ_API uint64_t dgz_kernel_launches(void);
                                 shm_name must be NULL (share it across processes with dgz_host_export /
                                 dgz_host_import). */
 
+#define DGZ_HOST_MANAGED 128u /* CUDA managed memory kept in HOST memory: cudaMallocManaged +
+                                 cudaMemAdviseSetPreferredLocation(CPU) before first touch, so the CPU
+                                 fills it in place and it never migrates; dgz_register_table then maps
+                                 it for the GPU (cudaMemAdviseSetAccessedBy) and the gather reads it by
+                                 zero-copy like a registered table.  The driver maps such memory with
+                                 large GPU pages, so sparse rows are not bound by the GPU page walks a
+                                 cudaHostRegister'd table pays per 64 KiB.
+                                 Needs a CUDA device; shm_name must be NULL (managed memory is not
+                                 shareable across processes: one copy per process). */
+
 /* Number of NUMA nodes this process may allocate on (cpuset Mems_allowed; 1 when unknown). */
 DGZ_API int dgz_host_numa_nodes(void);
 /* Map `bytes` of host memory.  shm_name == NULL: private anonymous mapping.  Otherwise a POSIX
@@ -114,6 +124,10 @@ DGZ_API dgz_status dgz_host_import(int fd, size_t bytes, void** ptr);
 #define DGZ_REG_DEVICE 16u    /* (reported) a device-resident table wrapped by dgz_wrap_device_table */
 #define DGZ_REG_VMM_BACKED 8u /* (reported in dgz_table_info.flags) the table lies in a DGZ_HOST_VMM
                                  allocation: no cudaHostRegister, mapped by the VMM allocation itself */
+#define DGZ_REG_MANAGED 32u   /* (reported) the table lies in CUDA managed memory (e.g. DGZ_HOST_MANAGED):
+                                 no cudaHostRegister; registration advises AccessedBy(current device)
+                                 so the GPU reads the host-resident pages through its own mapping, and a
+                                 gather on another device adds that device on first use */
 
 /* host_ptr: row 0 of a row-major, unpadded rows x dim table of `dtype` elements in host
  * memory (any alignment; unaligned bases are a first-class case, S:37 base_offset).  The caller

@@ -61,6 +61,7 @@ using namespace dgz;
 static std::mutex g_pinned_mu;
 static std::map<uintptr_t, size_t> g_pinned;  // cudaHostAlloc'ed host tables -> bytes
 static std::map<uintptr_t, size_t> g_mapped;  // hugetlb mappings -> mapped (rounded) bytes
+static std::map<uintptr_t, size_t> g_managed; // DGZ_HOST_MANAGED allocations -> bytes
 
 dgz_status dgz_vmm_alloc(size_t bytes, void** ptr);
 int dgz_vmm_free(void* ptr);
@@ -122,6 +123,23 @@ extern "C" dgz_status dgz_host_alloc(const char* shm_name, size_t bytes, int cre
     if (flags & DGZ_HOST_VMM) {
         DGZ_REQUIRE(!shm_name, "dgz_host_alloc: DGZ_HOST_VMM allocations are shared with dgz_host_export, not by name");
         return dgz_vmm_alloc(bytes, ptr);
+    }
+    if (flags & DGZ_HOST_MANAGED) {
+        DGZ_REQUIRE(!shm_name, "dgz_host_alloc: DGZ_HOST_MANAGED memory cannot be named (not shareable across processes)");
+        void* p = nullptr;
+        cudaError_t e = cudaMallocManaged(&p, bytes, cudaMemAttachGlobal);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocManaged");
+        // before the first touch: the CPU's writes then place every page in host memory, and no GPU
+        // access migrates it (the GPU gets a mapping at registration, dgz_register_table)
+        e = cudaMemAdvise(p, bytes, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return cuda_fail(e, "cudaMemAdvise(PreferredLocation = CPU)");
+        }
+        std::lock_guard<std::mutex> g(g_pinned_mu);
+        g_managed[(uintptr_t)p] = bytes;
+        *ptr = p;
+        return DGZ_OK;
     }
     if (flags & DGZ_HOST_CUDA_PINNED) {
         DGZ_REQUIRE(!shm_name, "dgz_host_alloc: DGZ_HOST_CUDA_PINNED memory cannot be named");
@@ -206,6 +224,11 @@ extern "C" dgz_status dgz_host_free(void* ptr, size_t bytes) {
             if (e != cudaSuccess) return cuda_fail(e, "cudaFreeHost");
             return DGZ_OK;
         }
+        if (g_managed.erase((uintptr_t)ptr)) {
+            cudaError_t e = cudaFree(ptr);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFree (managed)");
+            return DGZ_OK;
+        }
     }
     {
         std::lock_guard<std::mutex> g(g_pinned_mu);
@@ -287,8 +310,20 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
         delete t;
         return (dgz_status)(-vmm);
     }
+    cudaPointerAttributes pa{};
+    const bool managed = vmm != 1 && cudaPointerGetAttributes(&pa, host_ptr) == cudaSuccess && pa.type == cudaMemoryTypeManaged;
+    cudaGetLastError();
     if (vmm == 1) {
         t->flags |= DGZ_REG_NO_PIN | DGZ_REG_VMM_BACKED;  // CUDA VMM host memory: already mapped
+    } else if (managed) {
+        // CUDA managed memory: no page locking by us; the current device gets a mapping of the pages
+        // where they are (host memory for DGZ_HOST_MANAGED), read by the gather like a registered table
+        t->flags |= DGZ_REG_NO_PIN | DGZ_REG_MANAGED;
+        e = cudaMemAdvise(host_ptr, bytes, cudaMemAdviseSetAccessedBy, t->device);
+        if (e != cudaSuccess) {
+            delete t;
+            return cuda_fail(e, "cudaMemAdvise(AccessedBy)");
+        }
     } else if (!(flags & DGZ_REG_NO_PIN) && !is_cuda_pinned(host_ptr)) {
         unsigned int rf = cudaHostRegisterMapped;
         if (flags & DGZ_REG_PORTABLE) rf |= cudaHostRegisterPortable;
@@ -332,8 +367,8 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
         }
     }
     t->register_seconds = now_s() - t0;
-    void* dptr = (void*)host_ptr;  // VMM host memory: one VA for the CPU and every GPU
-    e = vmm == 1 ? cudaSuccess : cudaHostGetDevicePointer(&dptr, (void*)host_ptr, 0);
+    void* dptr = (void*)host_ptr;  // VMM / managed memory: one VA for the CPU and every GPU
+    e = (vmm == 1 || managed) ? cudaSuccess : cudaHostGetDevicePointer(&dptr, (void*)host_ptr, 0);
     if (e != cudaSuccess) {
         if (t->reg_base) cudaHostUnregister(t->reg_base);
         delete t;

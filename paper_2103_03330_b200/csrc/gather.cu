@@ -514,6 +514,9 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
             set_error("dgz_gather: VMM table not accessible from device %d", dev);
             return DGZ_ERR_STATE;
         }
+    } else if (dev != t->device && (t->flags & DGZ_REG_MANAGED)) {
+        // managed memory is mapped only into the devices advised AccessedBy: add this one (idempotent)
+        DGZ_CUDA(cudaMemAdvise(t->host, (size_t)t->rows * (size_t)t->row_bytes, cudaMemAdviseSetAccessedBy, dev));
     } else if (dev != t->device && !(t->flags & DGZ_REG_PORTABLE)) {
         set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
         return DGZ_ERR_STATE;

@@ -23,9 +23,10 @@ _lib = ctypes.CDLL(_SO)
 # --- constants (dgz.h) -------------------------------------------------------------------------
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_RANGE, ERR_STATE = range(6)
 F32, F16, BF16, U8 = range(4)
-REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED, REG_DEVICE = 1, 2, 4, 8, 16
+REG_PORTABLE, REG_READONLY, REG_NO_PIN, REG_VMM_BACKED, REG_DEVICE, REG_MANAGED = 1, 2, 4, 8, 16, 32
 HOST_HUGEPAGE, HOST_POPULATE, HOST_VMM, HOST_CUDA_PINNED, HOST_HUGETLB_2M, HOST_HUGETLB_1G = 1, 2, 4, 8, 16, 32
 HOST_NUMA_INTERLEAVE = 64
+HOST_MANAGED = 128
 GATHER_AUTO, GATHER_SEGMENT, GATHER_NAIVE, GATHER_SHIFT, GATHER_BULK = range(5)
 SCHED_AUTO, SCHED_INTERLEAVED, SCHED_BLOCKED = range(3)
 FLAG_NO_MERGE, FLAG_DEEP, FLAG_ORDER, FLAG_STREAM_STORES, FLAG_EVICT_FIRST_LOADS, FLAG_DYNAMIC = 1, 2, 4, 8, 16, 32

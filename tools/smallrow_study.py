@@ -26,7 +26,8 @@ torch.cuda.set_device(0)
 NCU = "--ncu" in sys.argv
 parts = [a for a in sys.argv[1:] if a in ("A", "B")] or ["A", "B"]
 total = gen.CONFIGS[4].table_bytes
-buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_HUGEPAGE)
+MANAGED = "--managed" in sys.argv    # the table in DGZ_HOST_MANAGED memory instead of cudaHostRegister'd
+buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_MANAGED if MANAGED else dgz.HOST_HUGEPAGE)
 gen.fill_table(buf.ptr, total, 9)
 outd = torch.empty((256 << 20) + 4096, dtype=torch.uint8, device="cuda")
 a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -67,7 +68,7 @@ if "A" in parts:
             if rep == 0 and not NCU:
                 continue      # first list warms the code path; report the second (fresh pages too)
             h = ids.cpu().numpy() * R
-            rec = {"part": "A", "R": R, "stride": s, "n": n, "gbs": round(n * R / t / 1e9, 2), "mrows_s": round(n / t / 1e6, 1),
+            rec = {"part": "A", "table": "managed" if MANAGED else "registered", "R": R, "stride": s, "n": n, "gbs": round(n * R / t / 1e9, 2), "mrows_s": round(n / t / 1e6, 1),
                    "pages4k": distinct(h, 12), "regions64k": distinct(h, 16), "regions2m": distinct(h, 21), "ms": round(t * 1e3, 3)}
             rec["m_pages4k_s"] = round(rec["pages4k"] / t / 1e6, 1)
             rec["m_regions64k_s"] = round(rec["regions64k"] / t / 1e6, 1)
@@ -93,7 +94,7 @@ if "B" in parts:
                 h = srt.cpu().numpy() * R
                 counts = {"pages4k": distinct(h, 12), "regions64k": distinct(h, 16), "regions2m": distinct(h, 21)}
         t = float(np.median(res))
-        rec = {"part": "B", "R": R, "n": n, "gbs": round(n * R / t / 1e9, 2), "mrows_s": round(n / t / 1e6, 1),
+        rec = {"part": "B", "table": "managed" if MANAGED else "registered", "R": R, "n": n, "gbs": round(n * R / t / 1e9, 2), "mrows_s": round(n / t / 1e6, 1),
                "ms": round(t * 1e3, 3), **counts}
         rec["m_pages4k_s"] = round(counts["pages4k"] / t / 1e6, 1)
         rec["m_regions64k_s"] = round(counts["regions64k"] / t / 1e6, 1)
