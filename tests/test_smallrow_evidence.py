@@ -65,13 +65,14 @@ def test_walk_traffic_per_region():
 
 
 def test_walk_model_predicts_the_config4_gather():
-    """The headline kernel sits on the same walker bound: a config-4 minibatch (the bench's last
+    """The config-4 gather from a registered table sits on the same walker bound: a minibatch (the bench's last
     timed batches, recomputed here by the oracle) touches ~0.53 M distinct 64 KiB regions of the
     56.9 GB table; at the walk rate measured on random lists that is the measured gather time."""
     import numpy as np
     import dgz_inputs as gen
     import oracle
-    line = json.load(open(os.path.join(P, "bench_config4.json")))
+    line = json.load(open(os.path.join(P, "bench_config4_registered.json")))   # the cudaHostRegister'd table
+    assert line["config"]["host_table"] == "registered"
     c = gen.CONFIGS[4]
     off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
     regions = []
@@ -87,3 +88,27 @@ def test_walk_model_predicts_the_config4_gather():
     t_meas = line["roofline"]["gather_ms_mean"]
     assert 0.5e6 < np.mean(regions) < 0.56e6
     assert abs(t_walk_ms - t_meas) / t_meas < 0.08, (t_walk_ms, t_meas)
+
+
+def test_managed_table_removes_the_walks():
+    """The same study on a DGZ_HOST_MANAGED table (profiles/r02/smallrow_study_managed.jsonl,
+    smallrow_ncu_managed.csv): the page-walk traffic is gone -- DRAM reads are the IDs and the inverse
+    permutation (16 B per row) and nothing else -- and 128 / 256 B random rows run at the link's
+    request rate instead of the walk rate (about 2x and 1.7x the registered table)."""
+    P2 = os.path.join(ROOT, "profiles", "r02")
+    man = [json.loads(l) for l in open(os.path.join(P2, "smallrow_study_managed.jsonl"))]
+    reg = [json.loads(l) for l in open(os.path.join(P2, "smallrow_study.jsonl"))]
+    mb = {t["R"]: t for t in man if t["part"] == "B"}
+    rb = {t["R"]: t for t in reg if t["part"] == "B"}
+    assert mb[128]["gbs"] > 40 and mb[128]["gbs"] > 1.8 * rb[128]["gbs"]
+    assert mb[256]["gbs"] > 1.5 * rb[256]["gbs"] and mb[512]["gbs"] >= 0.98 * rb[512]["gbs"]
+    # 64 KiB regions per second far above the registered table's walk rate
+    assert mb[128]["m_regions64k_s"] > 1.8 * rb[128]["m_regions64k_s"]
+    launches = smallrow_summary.ncu_launches(os.path.join(P2, "smallrow_ncu_managed.csv"))
+    for t, m in zip([t for t in man if t["part"] == "B"], launches):
+        assert abs(m["dram__bytes_read.sum"] - 16 * t["n"]) / (16 * t["n"]) < 0.05, (t["R"], m["dram__bytes_read.sum"])
+        assert m["syslts__t_sectors_srcunit_tex_aperture_sysmem_op_read_lookup_miss.sum"] == t["n"] * t["R"] // 32
+    # fixed strides: no collapse at 64 KiB any more (the unit is 2 MiB pages)
+    ma = {t["stride"]: t for t in man if t["part"] == "A"}
+    ra = {t["stride"]: t for t in reg if t["part"] == "A"}
+    assert ma[65536]["mrows_s"] > 3.5 * ra[65536]["mrows_s"] and ma[131072]["mrows_s"] > 3.5 * ra[131072]["mrows_s"]

@@ -27,6 +27,7 @@ NCU = "--ncu" in sys.argv
 parts = [a for a in sys.argv[1:] if a in ("A", "B")] or ["A", "B"]
 total = gen.CONFIGS[4].table_bytes
 MANAGED = "--managed" in sys.argv    # the table in DGZ_HOST_MANAGED memory instead of cudaHostRegister'd
+UNSORTED = "--unsorted" in sys.argv  # part B without the address sort
 buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_MANAGED if MANAGED else dgz.HOST_HUGEPAGE)
 gen.fill_table(buf.ptr, total, 9)
 outd = torch.empty((256 << 20) + 4096, dtype=torch.uint8, device="cuda")
@@ -86,7 +87,10 @@ if "B" in parts:
         res = []
         for rep in range(1 if NCU else 3):
             ids = torch.from_numpy(gen.distinct_ids(rows, n, R * 31 + rep)).cuda()
-            srt, pos = orderer.order(ids, rows)
+            if UNSORTED:     # the list as drawn (no address order): positions are the identity
+                srt, pos = ids, torch.arange(n, dtype=torch.int64, device="cuda")
+            else:
+                srt, pos = orderer.order(ids, rows)
             torch.cuda.synchronize()
             t = timed(tb, srt, pos, n)
             res.append(t)
@@ -94,7 +98,7 @@ if "B" in parts:
                 h = srt.cpu().numpy() * R
                 counts = {"pages4k": distinct(h, 12), "regions64k": distinct(h, 16), "regions2m": distinct(h, 21)}
         t = float(np.median(res))
-        rec = {"part": "B", "table": "managed" if MANAGED else "registered", "R": R, "n": n, "gbs": round(n * R / t / 1e9, 2), "mrows_s": round(n / t / 1e6, 1),
+        rec = {"part": "B", "table": "managed" if MANAGED else "registered", "sorted": not UNSORTED, "R": R, "n": n, "gbs": round(n * R / t / 1e9, 2), "mrows_s": round(n / t / 1e6, 1),
                "ms": round(t * 1e3, 3), **counts}
         rec["m_pages4k_s"] = round(counts["pages4k"] / t / 1e6, 1)
         rec["m_regions64k_s"] = round(counts["regions64k"] / t / 1e6, 1)
