@@ -341,6 +341,8 @@ def main():
     ap.add_argument("--fetch-warps", type=int, default=2,
                     help="warps per SM of the partition's gather (few: beside training the page walks slow down)")
     ap.add_argument("--threads", type=int, default=max(1, (os.cpu_count() or 2) - 1))   # one core left for the training loop
+    ap.add_argument("--host-table", default="registered", choices=["registered", "managed"],
+                    help="zc mode's host table: cudaHostRegister'd (the paper's) or DGZ_HOST_MANAGED")
     ap.add_argument("--dump", default=None,
                     help="directory: write the first zc minibatch and the last DMA minibatch of each rank as .npz")
     a = ap.parse_args()
@@ -360,7 +362,10 @@ def main():
         import dataclasses
         c = dataclasses.replace(c, dim=a.dim)
     K = a.steps
-    if G == 1:
+    if a.host_table == "managed":   # one DGZ_HOST_MANAGED copy per rank (2 MiB GPU pages)
+        buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_MANAGED)
+        gen.fill_table(buf.ptr, c.table_bytes, c.seed)
+    elif G == 1:
         buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_HUGEPAGE)
         gen.fill_table(buf.ptr, c.table_bytes, c.seed)
     else:   # one host table per box, registered by every rank
@@ -379,7 +384,7 @@ def main():
     batches = [i * G + rank for i in range(K + 2)]          # seed partition: global batch j = i*G + rank
     seeds = [torch.from_numpy(gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)).cuda() for j in batches]
     rng = [gen.batch_rng_seed(c.seed, j) for j in batches]
-    res = {"config": c.name, "dim": c.dim, "steps": K, "ranks": G, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
+    res = {"config": c.name, "dim": c.dim, "steps": K, "ranks": G, "host_table": a.host_table, "model": f"GraphSAGE-mean {len(c.fanouts)} layers, hidden {a.hidden}, "
                                                               f"{a.classes} classes, Adam, fp32 (TF32 matmuls)"
                                                               + (", DDP" if G > 1 else "")}
     modes = a.modes.split(",")
