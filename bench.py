@@ -329,15 +329,13 @@ HOST_TABLE_POLICY = {
 def host_table_kind(args, d: Dist, nbytes: int) -> str:
     """'managed' (DGZ_HOST_MANAGED: CUDA managed memory kept in host memory, mapped for the GPU with
     large pages -- DESIGN.md 5.1) or 'registered' (the paper's cudaHostRegister'd table, one shared
-    /dev/shm copy per box).  auto: managed when every rank can hold its own copy in host
-    RAM (managed memory is not shareable across processes), else registered.  Collective."""
+    /dev/shm copy per box).  auto: managed for one process; registered for N > 1 ranks
+    (managed memory is not shareable across processes, and two processes allocating a 57 GB managed
+    table each on one box failed in cudaMallocManaged here) -- `--host-table managed` forces one copy
+    per rank."""
     kind = args.host_table
     if kind == "auto":
-        kind = "managed"
-        if d.world > 1:
-            avail = _meminfo_bytes("MemAvailable") or 0
-            kind = "managed" if d.world * nbytes <= 0.7 * avail else "registered"
-            kind = d.bcast_obj(kind)
+        kind = "managed" if d.world == 1 else "registered"
     return kind
 
 
