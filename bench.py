@@ -348,6 +348,26 @@ def make_table(cfg, d: Dist, dgz, kind: str = "registered"):
         t0 = time.time()
         gen.fill_table(buf.ptr, nbytes, cfg.seed)
         return buf, time.time() - t0
+    return make_registered_table(cfg, d, dgz)
+
+
+def make_table_kind(cfg, d: Dist, dgz, kind: str):
+    """make_table, falling back to the registered table when a managed allocation fails (N = 1 only:
+    with N > 1 every rank must use the same kind).  Returns (buffer, fill seconds, kind used)."""
+    if kind == "managed" and d.world == 1:
+        try:
+            buf, fill_s = make_table(cfg, d, dgz, "managed")
+            return buf, fill_s, "managed"
+        except Exception as e:   # DgzError from cudaMallocManaged / cudaMemAdvise
+            print(f"# managed host table unavailable ({str(e)[:160]}); using the registered table", file=sys.stderr)
+            buf, fill_s = make_table(cfg, d, dgz, "registered")
+            return buf, fill_s, "registered (managed allocation failed)"
+    buf, fill_s = make_table(cfg, d, dgz, kind)
+    return buf, fill_s, kind
+
+
+def make_registered_table(cfg, d: Dist, dgz):
+    nbytes = cfg.table_bytes
     if d.world == 1:
         buf = dgz.HostBuffer(nbytes + 4096, flags=dgz.HOST_HUGEPAGE)
         t0 = time.time()
@@ -564,7 +584,7 @@ def run_ours(args, d: Dist):
                     2 * bound * R + (3 << 30) + (csr_bytes if G == 1 else 0) + per_rank_tab)
     t_setup = time.time()
     gen.set_threads(max(1, (os.cpu_count() or 1) // G))
-    buf, fill_s = make_table(cfg, d, dgz, tkind)
+    buf, fill_s, tkind = make_table_kind(cfg, d, dgz, tkind)
     d.barrier()
     table = dgz.register_table(buf.ptr, cfg.n_nodes, cfg.dim, dgz.F32)
     info = table.info
@@ -676,7 +696,7 @@ def run_ours(args, d: Dist):
     cpu_base = dma_base = parity = None
     cpus, node = rank_cpu_share(d)
     if not args.no_baselines:
-        bt = baseline_table(dgz, buf, cfg.table_bytes, cfg.seed, tkind == "managed" and G == 1)
+        bt = baseline_table(dgz, buf, cfg.table_bytes, cfg.seed, tkind.startswith("managed") and G == 1)
         dma_base = run_dma_baseline(cfg, bt.buf, fetcher, seeds_dev, rng, K, d, cpus, node)
         dma_base["host_table"] = bt.what
         bt.close()
@@ -752,8 +772,9 @@ def run_ours(args, d: Dist):
                   "mapping_ratio": round(cfg.table_bytes / max(info.gpu_mem_delta, 1), 1),
                   "csr_gen_s": round(csr_s, 2), "total_s": round(time.time() - t_setup, 1), "sms": sm_count,
                   "host_numa_nodes": dgz.host_numa_nodes(), "preflight": pre,
-                  "host_table_policy": HOST_TABLE_POLICY[tkind] if tkind == "managed" or G > 1 else
-                                       "anonymous THP mapping (first touch), cudaHostRegister"},
+                  "host_table_policy": (HOST_TABLE_POLICY["managed"] if tkind == "managed" else
+                                        HOST_TABLE_POLICY["registered"] if G > 1 else
+                                        "anonymous THP mapping (first touch), cudaHostRegister")},
     }
     fetcher.close()
     if cache is not None and G > 1:
@@ -1259,7 +1280,7 @@ def run_rowsweep(args, d: Dist):
                     2 * (W + K) * n * 8 + 2 * (32 << 20) + (3 << 30) + (total if tkind == "managed" else 0))
     t_setup = time.time()
     gen.set_threads(max(1, (os.cpu_count() or 1) // G))
-    buf, fill_s = make_table(c4, d, dgz, tkind)
+    buf, fill_s, tkind = make_table_kind(c4, d, dgz, tkind)
     d.barrier()
     table = dgz.register_table(buf.ptr + base, rows, R // eb, dtype)
     info = table.info
