@@ -886,8 +886,8 @@ def run_e2e(fetcher, cfg, seeds_host, rng, W, K, d: Dist):
 OVERLAP_CANDIDATES = ((32, True, 2, "partition"), (24, True, 2, "partition"), (40, True, 2, "partition"),
                       (16, True, 4, "partition"), (48, True, 1, "partition"), (24, False, 2, "partition"),
                       (8, True, 8, "partition"),
-                      (24, True, 2, "whole GPU"), (32, True, 2, "whole GPU"), (48, True, 1, "whole GPU"),
-                      (64, True, 1, "whole GPU"), (74, True, 1, "whole GPU"), (96, True, 1, "whole GPU"))
+                      (16, True, 4, "whole GPU"), (24, True, 2, "whole GPU"), (32, True, 2, "whole GPU"),
+                      (48, True, 1, "whole GPU"), (64, True, 1, "whole GPU"), (74, True, 1, "whole GPU"))
 
 
 def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
@@ -1014,7 +1014,8 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
         # lane, few warps per SM: beside a DRAM-heavy consumer the page walks slow down and fewer rows in
         # flight win.  Sampler placement x consumer placement, all measured.
         combos = ((("fetch partition", "partition"), ("consumer stream", "partition")) if placement == "partition"
-                  else (("fetch partition", "whole GPU"), ("own 8-SM partition", "whole GPU")))
+                  else (("fetch partition", "whole GPU"), ("consumer stream", "whole GPU"),
+                        ("own 8-SM partition", "whole GPU")))
         for where, cons in combos:
             if where == "own 8-SM partition" and not spread:
                 continue
