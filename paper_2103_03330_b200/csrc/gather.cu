@@ -427,7 +427,15 @@ static LaunchPlan plan_launch(const dgz_table_s* t, int64_t n, bool sorted_path,
         (flags & ~(DGZ_GATHER_FLAG_NO_MERGE | DGZ_GATHER_FLAG_STREAM_STORES | DGZ_GATHER_FLAG_EVICT_FIRST_LOADS |
                    DGZ_GATHER_FLAG_DYNAMIC)) == 0) {
         flags |= DGZ_GATHER_FLAG_DEEP;
-        if (variant == DGZ_GATHER_SEGMENT && !cache) {
+        if (variant == DGZ_GATHER_SEGMENT && !cache && (t->flags & DGZ_REG_MANAGED)) {
+            // managed host table (2 MiB GPU pages, no page-walk bound; DESIGN.md 5.1,
+            // tools/managed_shape_sweep.py): rows of one line are bound by the link's request rate
+            // and want one warp per SM; rows of >= 2 lines reach the link with 4 (256 B random rows
+            // 48.1 -> 50.9 GB/s, 512 B 49.1 -> 51.0)
+            const int64_t lines = (t->row_bytes + 127) / 128;
+            k = nsm;
+            warps = lines >= 2 ? 4 : 1;
+        } else if (variant == DGZ_GATHER_SEGMENT && !cache) {
             // Translation-bound regime (explore19-22): below ~1 KiB per row
             // the rate is set by GPU page walks, and it peaks with FEWER rows (distinct pages) in
             // flight than the 2-warps-per-SM shape that dense 512 B minibatches want.  Measured rule

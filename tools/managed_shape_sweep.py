@@ -30,7 +30,8 @@ for R in (64, 128, 256, 512, 2048):
     tb = dgz.register_table(buf.ptr, rows, R // 4, dgz.F32)
     orderer = dgz.Orderer(n)
     default = dgz.gather_plan(tb, n, True)
-    for k, w, cps, fl in [None] + SHAPES:
+    for shp in [None] + SHAPES:
+        k, w, cps, fl = shp if shp is not None else (None, 0, 0, 0)
         cfg = None if k is None else dgz.gather_cfg(sm_count=k, warps_per_cta=w, ctas_per_sm=cps, flags=fl)
         ts = []
         for rep in range(3):
