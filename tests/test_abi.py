@@ -86,3 +86,25 @@ def test_numa_interleaved_host_allocation():
         a.free()
         b.unlink()
         b.free()
+
+
+def test_binding_constants_match_the_header():
+    """Every flag the binding exposes has the value include/dgz.h defines (HOST_*, REG_*, FLAG_*)."""
+    from paper_2103_03330_b200 import dgz
+    src = open(os.path.join(ROOT, "include", "dgz.h")).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+DGZ_(\w+)\s+(\d+)u?\b", src)}
+    pairs = {"HOST_HUGEPAGE": "HOST_HUGEPAGE", "HOST_POPULATE": "HOST_POPULATE", "HOST_VMM": "HOST_VMM",
+             "HOST_CUDA_PINNED": "HOST_CUDA_PINNED", "HOST_HUGETLB_2M": "HOST_HUGETLB_2M",
+             "HOST_HUGETLB_1G": "HOST_HUGETLB_1G", "HOST_NUMA_INTERLEAVE": "HOST_NUMA_INTERLEAVE",
+             "HOST_MANAGED": "HOST_MANAGED", "REG_PORTABLE": "REG_PORTABLE", "REG_READONLY": "REG_READONLY",
+             "REG_NO_PIN": "REG_NO_PIN", "REG_VMM_BACKED": "REG_VMM_BACKED", "REG_DEVICE": "REG_DEVICE",
+             "REG_MANAGED": "REG_MANAGED", "GATHER_FLAG_NO_MERGE": "FLAG_NO_MERGE", "GATHER_FLAG_DEEP": "FLAG_DEEP",
+             "GATHER_FLAG_ORDER": "FLAG_ORDER", "GATHER_FLAG_STREAM_STORES": "FLAG_STREAM_STORES",
+             "GATHER_FLAG_EVICT_FIRST_LOADS": "FLAG_EVICT_FIRST_LOADS", "GATHER_FLAG_DYNAMIC": "FLAG_DYNAMIC"}
+    for h, py in pairs.items():
+        assert h in defs, h
+        assert getattr(dgz, py) == defs[h], (h, defs[h], getattr(dgz, py))
+    # flag bits of one family never collide
+    for fam in ("HOST_", "REG_", "GATHER_FLAG_"):
+        vals = [v for k, v in defs.items() if k.startswith(fam)]
+        assert len(vals) == len(set(vals)), fam

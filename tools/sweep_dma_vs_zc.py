@@ -26,9 +26,14 @@ for a in sys.argv[1:]:
         threads = int(a.split("=", 1)[1])
 torch.set_num_threads(threads)
 total = gen.CONFIGS[4].table_bytes
-buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_HUGEPAGE)
+MANAGED = "--managed" in sys.argv   # zero-copy from a DGZ_HOST_MANAGED table; the CPU gather reads a THP copy
+buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_MANAGED if MANAGED else dgz.HOST_HUGEPAGE)
 gen.fill_table(buf.ptr, total + 4096, 9)
-host_all = torch.from_numpy(buf.numpy(0, total + 4096))
+cpu_buf = buf
+if MANAGED:
+    cpu_buf = dgz.HostBuffer(total + 4096, flags=dgz.HOST_HUGEPAGE)
+    gen.fill_table(cpu_buf.ptr, total + 4096, 9)
+host_all = torch.from_numpy(cpu_buf.numpy(0, total + 4096))
 outd = torch.empty((256 << 20) + 4096, dtype=torch.uint8, device="cuda")
 CH = 32 << 20
 stage = [torch.empty(CH + 4096, dtype=torch.uint8).pin_memory() for _ in range(2)]
@@ -77,7 +82,8 @@ for R in WIDTHS:
         b.record()
         torch.cuda.synchronize()
         t_zc = a.elapsed_time(b) / 3 * 1e-3
-        rec = {"R": R, "base": base, "n": n, "zc_gbs": round(n * R / t_zc / 1e9, 2), "zc_mrows_s": round(n / t_zc / 1e6, 1)}
+        rec = {"R": R, "base": base, "n": n, "table": "managed" if MANAGED else "registered",
+               "zc_gbs": round(n * R / t_zc / 1e9, 2), "zc_mrows_s": round(n / t_zc / 1e6, 1)}
         if "--zc-only" not in sys.argv:
             # dma baseline on the same IDs
             host_rows = host_all[base:base + rows * R].view(rows, R)
@@ -91,3 +97,5 @@ for R in WIDTHS:
         print(json.dumps(rec), flush=True)
         tb.unregister()
 buf.free()
+if cpu_buf is not buf:
+    cpu_buf.free()
