@@ -324,6 +324,7 @@ extern "C" dgz_status dgz_register_table(const void* host_ptr, int64_t rows, int
             delete t;
             return cuda_fail(e, "cudaMemAdvise(AccessedBy)");
         }
+        if (t->device >= 0 && t->device < 64) t->managed_devs = uint64_t(1) << t->device;
     } else if (!(flags & DGZ_REG_NO_PIN) && !is_cuda_pinned(host_ptr)) {
         unsigned int rf = cudaHostRegisterMapped;
         if (flags & DGZ_REG_PORTABLE) rf |= cudaHostRegisterPortable;

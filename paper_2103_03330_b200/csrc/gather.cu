@@ -523,8 +523,13 @@ dgz_status dgz_gather_impl(dgz_table t, const void* idx, int idx_is64, const int
             return DGZ_ERR_STATE;
         }
     } else if (dev != t->device && (t->flags & DGZ_REG_MANAGED)) {
-        // managed memory is mapped only into the devices advised AccessedBy: add this one (idempotent)
-        DGZ_CUDA(cudaMemAdvise(t->host, (size_t)t->rows * (size_t)t->row_bytes, cudaMemAdviseSetAccessedBy, dev));
+        // managed memory is mapped only into the devices advised AccessedBy: add this one on its
+        // first gather (the bit is set after the advice succeeded; a race only repeats the advice)
+        const uint64_t bit = dev < 64 ? uint64_t(1) << dev : 0;
+        if (!(__atomic_load_n(&t->managed_devs, __ATOMIC_ACQUIRE) & bit)) {
+            DGZ_CUDA(cudaMemAdvise(t->host, (size_t)t->rows * (size_t)t->row_bytes, cudaMemAdviseSetAccessedBy, dev));
+            __atomic_fetch_or(&t->managed_devs, bit, __ATOMIC_RELEASE);
+        }
     } else if (dev != t->device && !(t->flags & DGZ_REG_PORTABLE)) {
         set_error("dgz_gather: table registered on device %d without DGZ_REG_PORTABLE, current device %d", t->device, dev);
         return DGZ_ERR_STATE;

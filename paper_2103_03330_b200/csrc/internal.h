@@ -46,6 +46,7 @@ struct dgz_table_s {
     int64_t gpu_mem_delta;
     double register_seconds;
     int* err_flag[64];        // per-device RANGE flag (device memory), lazily allocated
+    uint64_t managed_devs;    // DGZ_REG_MANAGED: devices already advised AccessedBy (bit d = device d)
 };
 
 // gather.cu
