@@ -108,3 +108,33 @@ def test_binding_constants_match_the_header():
     for fam in ("HOST_", "REG_", "GATHER_FLAG_"):
         vals = [v for k, v in defs.items() if k.startswith(fam)]
         assert len(vals) == len(set(vals)), fam
+
+
+def test_host_alloc_path_names(tmp_path):
+    """dgz_host_alloc with a path instead of a /dev/shm name: a file (created and truncated here)
+    and another process's memfd reached through /proc/<pid>/fd/<n> -- the bench's fallback when
+    /dev/shm is too small for the shared table.  CPU only."""
+    from paper_2103_03330_b200 import dgz
+    path = str(tmp_path / "table.bin")
+    a = dgz.HostBuffer(1 << 16, path, create=True, flags=0)
+    try:
+        a.numpy()[:8] = list(range(1, 9))
+        b = dgz.HostBuffer(1 << 16, path, create=False, flags=0)
+        assert list(b.numpy()[:8]) == list(range(1, 9))       # the same pages through a second mapping
+        b.free()
+        a.unlink()
+        assert not os.path.exists(path)
+    finally:
+        a.free()
+    fd = os.memfd_create("dgz_abi_memfd", 0)
+    try:
+        os.ftruncate(fd, 1 << 16)
+        os.pwrite(fd, bytes([7, 7, 7]), 100)
+        m = dgz.HostBuffer(1 << 16, f"/proc/{os.getpid()}/fd/{fd}", create=False, flags=0)
+        assert list(m.numpy()[100:103]) == [7, 7, 7]
+        m.numpy()[200] = 9
+        assert os.pread(fd, 1, 200) == bytes([9])
+        m.unlink()                                               # a no-op for /proc paths
+        m.free()
+    finally:
+        os.close(fd)
