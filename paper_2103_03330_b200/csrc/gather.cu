@@ -427,11 +427,12 @@ static LaunchPlan plan_launch(const dgz_table_s* t, int64_t n, bool sorted_path,
         (flags & ~(DGZ_GATHER_FLAG_NO_MERGE | DGZ_GATHER_FLAG_STREAM_STORES | DGZ_GATHER_FLAG_EVICT_FIRST_LOADS |
                    DGZ_GATHER_FLAG_DYNAMIC)) == 0) {
         flags |= DGZ_GATHER_FLAG_DEEP;
-        if (variant == DGZ_GATHER_SEGMENT && !cache && (t->flags & DGZ_REG_MANAGED)) {
+        if (variant == DGZ_GATHER_SEGMENT && (t->flags & DGZ_REG_MANAGED)) {
             // managed host table (2 MiB GPU pages, no page-walk bound; DESIGN.md 5.1,
             // tools/managed_shape_sweep.py): rows of one line are bound by the link's request rate
             // and want one warp per SM; rows of >= 2 lines reach the link with 4 (256 B random rows
-            // 48.1 -> 50.9 GB/s, 512 B 49.1 -> 51.0)
+            // 48.1 -> 50.9 GB/s, 512 B 49.1 -> 51.0; cached gather, 20 % of the power-law graph in
+            // HBM: 103.5 -> 117.2 GB/s effective, tools/cache_managed_shapes.py)
             const int64_t lines = (t->row_bytes + 127) / 128;
             k = nsm;
             warps = lines >= 2 ? 4 : 1;
