@@ -709,7 +709,8 @@ def run_ours(args, d: Dist):
 
     clocks = clk.summary()
     sm_count = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    tkey = f"config{cfg.cid}" + (f"_cache{args.cache_frac:g}" if cache is not None else "")
+    tkey = (f"config{cfg.cid}" + ("_managed" if tkind == "managed" else "")
+            + (f"_cache{args.cache_frac:g}" if cache is not None else ""))
     traffic, traffic_detail, traffic_src = load_profile_traffic(tkey)
     peak = ceilings["h2d_dma_gbs"]
     per_rank = d.gather_obj({"rank": rank, "device": torch.cuda.current_device(), "numa_node": node,
