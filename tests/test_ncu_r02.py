@@ -33,3 +33,17 @@ def test_headline_capture_matches_oracle_and_walk_model():
     assert 110 < walk_bytes / regions < 210, walk_bytes / regions
     # and HBM writes = the rows (plus write-allocate noise): n * R within 15 %
     assert abs(cap["dram_write_bytes"] - n * c.row_bytes) / (n * c.row_bytes) < 0.15
+
+
+def test_managed_capture_has_no_walks():
+    """The same launch with the default managed host table (key config4_managed): the same sysmem
+    sectors (16 x |U|), and DRAM reads = the IDs and the inverse permutation only (16 B per row),
+    i.e. no page-walk traffic."""
+    with open(os.path.join(ROOT, "profiles", "r02", "ncu_gather_summary.json")) as f:
+        caps = json.load(f)
+    cap, reg = caps["config4_managed"], caps["config4"]
+    assert "managed" in cap["source"] and "launch 4" in cap["source"]
+    assert cap["sysmem_read_sectors"] == reg["sysmem_read_sectors"]          # the same minibatch (j = 0)
+    n = cap["sysmem_read_sectors"] // 16
+    assert abs(cap["dram_read_bytes"] - 16 * n) / (16 * n) < 0.05
+    assert reg["dram_read_bytes"] > 5 * cap["dram_read_bytes"]
