@@ -592,7 +592,10 @@ def run_ours(args, d: Dist):
     off, col, n_edges, csr_bufs = make_csr(cfg, d, dgz, skew_alpha=args.skew_alpha if args.cache_frac > 0 else 0.0)
     csr_s = time.time() - t0
     if args.csr == "host":    # zero-copy CSR (NEXT-3): the sampler reads the host arrays over PCIe
-        graph = dgz.HostGraph(off.ctypes.data, col.ctypes.data, cfg.n_nodes, n_edges, False)
+        if tkind == "managed":   # the columns in managed host memory too (2 MiB GPU pages)
+            graph = dgz.HostGraph(off, col, managed=True)
+        else:
+            graph = dgz.HostGraph(off.ctypes.data, col.ctypes.data, cfg.n_nodes, n_edges, False)
     else:                     # CSR replicated in each GPU's HBM
         graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
 
@@ -733,7 +736,8 @@ def run_ours(args, d: Dist):
                    "global_batch": cfg.batch * G, "parallelism": f"dp{G} (seed partition j mod G)",
                    "l2": "inputs larger than L2 (56.9 GB table, fresh minibatch every step)",
                    "pipeline": fetcher.mode, "pipeline_choice": choice,
-                   "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else "pinned host memory, sampled by zero-copy",
+                   "csr": "HBM (replicated per GPU)" if args.csr == "hbm" else
+                          f"host memory ({'managed' if tkind == 'managed' else 'registered'}), sampled by zero-copy",
                    "host_table": tkind,
                    "gather": dict(dgz.gather_plan(table, cap, True, gcfg),
                                   order="address-sorted + inverse permutation (dgz_gather_perm)"),

@@ -550,12 +550,15 @@ class HostGraph:
     dgz_csr -- no other change on the path.  By default the offsets (8 B per node, a small fraction
     of the columns) are copied to HBM, so the sampler's host page walks are for columns only.
     ``offsets`` / ``cols`` are host addresses (ints) of int64 [n_nodes + 1] and int32/int64
-    [n_edges] arrays the caller keeps alive, or numpy arrays (copied into HostBuffers here)."""
+    [n_edges] arrays the caller keeps alive, or numpy arrays (copied into HostBuffers here; with
+    ``managed=True`` into DGZ_HOST_MANAGED memory, which the GPU maps with 2 MiB pages)."""
 
     def __init__(self, offsets, cols, n_nodes: int | None = None, n_edges: int | None = None,
-                 cols_is64: bool | None = None, flags: int = REG_READONLY, offsets_in_hbm: bool = True):
+                 cols_is64: bool | None = None, flags: int = REG_READONLY, offsets_in_hbm: bool = True,
+                 managed: bool = False):
         import numpy as np
         self._owned = []
+        self._copy_flags = HOST_MANAGED if managed else HOST_HUGEPAGE   # numpy inputs: where the copies live
         self.offsets_dev = None
         if isinstance(offsets, np.ndarray):
             assert offsets.dtype == np.int64 and cols.dtype in (np.int32, np.int64)
@@ -590,7 +593,7 @@ class HostGraph:
 
     def _copy_in(self, a) -> int:
         import numpy as np
-        hb = HostBuffer(max(a.nbytes, 1))
+        hb = HostBuffer(max(a.nbytes, 1), flags=self._copy_flags)
         np.copyto(hb.numpy(0, a.nbytes).view(a.dtype), a)
         self._owned.append(hb)
         return hb.ptr

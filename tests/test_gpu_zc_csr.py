@@ -22,9 +22,9 @@ def dev():
     return torch.device("cuda", 0)
 
 
-def _compare(off, col, seeds, fanouts, rs, offsets_in_hbm=True):
+def _compare(off, col, seeds, fanouts, rs, offsets_in_hbm=True, managed=False):
     want = oracle.sample_uniform(off, col, seeds, fanouts, rs)
-    g = dgz.HostGraph(off, col, offsets_in_hbm=offsets_in_hbm)
+    g = dgz.HostGraph(off, col, offsets_in_hbm=offsets_in_hbm, managed=managed)
     try:
         bufs = dgz.SampleBuffers(g.n_nodes, max(len(seeds), 1), fanouts)
         dgz.sample_uniform(g, torch.from_numpy(np.asarray(seeds, dtype=np.int64)).cuda(), fanouts, rs, bufs)
@@ -49,9 +49,10 @@ def test_zero_copy_csr_sampler(dev, n, deg, fan, col64):
     off, col = gen.gen_csr(n, deg, n + 1)
     if col64:
         col = col.astype(np.int64)
-    for j, in_hbm in ((0, True), (5, False)):      # offsets in HBM (default) or also on the host
+    for j, in_hbm, managed in ((0, True, False), (5, False, False), (7, True, True), (9, False, True)):
+        # offsets in HBM (default) or also on the host; registered or managed host memory
         seeds = gen.batch_seeds(n, min(1024, n // 2), n + 1, j)
-        _compare(off, col, seeds, fan, gen.batch_rng_seed(n + 1, j), offsets_in_hbm=in_hbm)
+        _compare(off, col, seeds, fan, gen.batch_rng_seed(n + 1, j), offsets_in_hbm=in_hbm, managed=managed)
 
 
 def test_zero_copy_csr_edge_cases(dev):
