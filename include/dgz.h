@@ -369,6 +369,28 @@ DGZ_API dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int32_t
                               int32_t repeat, int32_t sm_count, int32_t ctas_per_sm, dgz_stream stream);
 
 /* ==========================================================================================
+ * Stand-in GraphSAGE layer (consumer, step a7: "mean over each dst node's sampled neighbours of
+ * the gathered rows, then a small GEMM" -- SURVEY 8(a) a7; P:554-555 fig:singlegpu; the layer
+ * P:224-229).  For dst node i < min(*n_dst_dev, n_dst_max):
+ *   h[i, :] = (x[i, :] + sum_{q < cnt[i]} x[nbr_local[i*fanout + q], :]) * (1 / (1 + cnt[i]))
+ *             (fp32, q in order: bit-identical to dgz_aggregate_mean)
+ *   y[i, n] = sum_k bf16(h[i, k]) * w[n*dim + k]    fp32 accumulation on the tensor cores
+ * x: fp32 [*, dim] device rows (the gathered minibatch), 4-byte aligned; w: bf16 [hidden, dim]
+ * device, row-major (nn.Linear weight layout), 2-byte aligned; y: fp32 [n_dst, hidden] device,
+ * 16-byte aligned, rows >= n_dst untouched.  hidden: a multiple of 16 in [16, 256]; (hidden + 128)
+ * x ceil16(dim) x 2 bytes must fit in shared memory (dim 128 / hidden 256: 96 KiB).  h is rounded
+ * to bf16 (round to nearest even) before the product: |y - h.W^T| <= 2^-8 sum_k |h_k w_nk| plus
+ * fp32 accumulation error.  repeat / sm_count / ctas_per_sm as for dgz_aggregate_mean.  Async on
+ * `stream`; n_dst_max == 0 is a no-op.  Errors: DGZ_ERR_INVALID (arguments, sizes), DGZ_ERR_CUDA.
+ * ========================================================================================== */
+DGZ_API dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const int32_t* nbr_local, const int32_t* cnt,
+                              int32_t fanout, const int64_t* n_dst_dev, int64_t n_dst_max, const void* w_bf16,
+                              int64_t hidden, float* y, int32_t repeat, int32_t sm_count, int32_t ctas_per_sm,
+                              dgz_stream stream);
+/* Shared-memory bytes (the two bf16 operands) and TMEM columns one dgz_sage_mean_linear CTA uses. */
+DGZ_API dgz_status dgz_sage_workspace(int64_t dim, int64_t hidden, int64_t* smem_bytes, int32_t* tmem_cols);
+
+/* ==========================================================================================
  * In-process SM partition (step a6): the paper's MPS X% / (100-X)% split done with
  * CUDA green contexts.  The current device's SMs are split into a fetch group of at least
  * `fetch_sms` SMs (rounded up to the hardware granularity: multiples of 8 on sm_90+, finer with

@@ -153,3 +153,25 @@ def sample_and_gather(off, col, seeds, fanouts, rng_seed, table_addr, rows, row_
         out = np.empty(n * row_bytes, dtype=np.uint8)
     gather_into(table_addr, rows, row_bytes, s.U, out)
     return s, out
+
+
+def sage_mean_linear(x: np.ndarray, local: np.ndarray, cnt: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """The consumer's layer, in fp64: Y = A_hat . H . W^T for the first n_dst = len(cnt)
+    rows, the paper's GCN layer H^(l+1) = A H^(l) W^(l) without the output non-linearity,
+    with A_hat the sampled block's row-normalised adjacency including the self edge (GraphSAGE mean
+    aggregation over the sampled neighbours):
+        A_hat[i, i] += 1 / (1 + cnt[i]),  A_hat[i, local[i, q]] += 1 / (1 + cnt[i])  for q < cnt[i].
+    x: [n_src, dim] rows of the minibatch (frontier order), local: [n_dst, fanout] positions in x,
+    cnt: [n_dst], w: [hidden, dim].  Written row by row: h_i = (x_i + sum_q x_local[i,q]) / (1 + cnt_i),
+    then Y = H . W^T (a library matmul as the second step)."""
+    x = np.asarray(x, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    cnt = np.asarray(cnt, dtype=np.int64)
+    n_dst = cnt.shape[0]
+    h = np.empty((n_dst, x.shape[1]), dtype=np.float64)
+    for i in range(n_dst):
+        s = x[i].copy()
+        for q in range(int(cnt[i])):
+            s += x[int(local[i, q])]
+        h[i] = s / (1.0 + cnt[i])
+    return h @ w.T

@@ -1,0 +1,272 @@
+// Stand-in GraphSAGE layer (the consumer of step a7; SURVEY 8(a) a7 "mean over each dst node's
+// sampled neighbours of the gathered rows, then a small GEMM"; P:554-555 fig:singlegpu
+// for the layer itself):
+//
+//   h[i, :] = (x[i, :] + sum_{q < cnt[i]} x[nbr_local[i*fanout + q], :]) * (1 / (1 + cnt[i]))   fp32
+//   y[i, :] = bf16(h[i, :]) . W^T            W: [hidden, dim] bf16 (nn.Linear layout), y fp32
+//
+// One CTA owns a tile of 128 destination nodes (the UMMA M):
+//   1. eight warps compute h for the tile from HBM (fp32, the same sequential order as
+//      dgz_aggregate_mean, so h is bit-identical to it), round it to bf16 and write it into shared
+//      memory as the K-major A operand (core-matrix layout, SWIZZLE_NONE);
+//   2. one thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = hidden, K = 16 per
+//      instruction, fp32 accumulate) with A and W from shared memory and D in tensor memory, and
+//      commits to an mbarrier;
+//   3. the eight warps read D back with tcgen05.ld (warp w: TMEM lanes 32(w%4).., column half w/4)
+//      and store y rows to HBM.
+// W is staged once per CTA in the same core-matrix layout (B operand, K-major).  The K dimension
+// is zero-padded to a multiple of 16.  Two CTAs share an SM (the TMEM columns and shared memory
+// are sized for it), so one CTA's MMA/epilogue overlaps the other's HBM-bound aggregation.
+#include "internal.h"
+
+#include <cuda_bf16.h>
+
+namespace {
+
+constexpr int kTileM = 128;
+constexpr int kThreads = 256;   // 8 warps
+constexpr int kWarps = kThreads / 32;
+
+// Core-matrix K-major layout of an [rows x Kp] bf16 operand (SWIZZLE_NONE, "interleave"):
+// element (r, k) at (r/8)*SBO + (k/8)*LBO + (r%8)*16 + (k%8)*2 with LBO = 128 B (the K-adjacent
+// 8x16 B core matrix) and SBO = Kp*16 B (the next 8 rows).
+__device__ __forceinline__ uint32_t core_off(int r, int k, int Kp) {
+    return (uint32_t)((r >> 3) * (Kp * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, int Kp) {
+    // bits 0-13 start >> 4, 16-29 LBO >> 4, 32-45 SBO >> 4, 46-47 version 1 (sm_100),
+    // 49-51 base offset 0, 52 LBO mode 0, 61-63 layout 0 = SWIZZLE_NONE
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)(((uint32_t)(Kp * 16) >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, N >> 3, M >> 4.
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int32_t* __restrict__ nbr,
+                        const int32_t* __restrict__ cnt, int fanout, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_max,
+                        const __nv_bfloat16* __restrict__ w, int N, uint32_t tmem_cols, float* __restrict__ y, int repeat,
+                        bool x_vec) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sB = smem;                                   // [N x Kp] bf16, core-matrix K-major
+    uint8_t* sA = smem + (size_t)N * Kp * 2;              // [128 x Kp] bf16
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sA + (size_t)kTileM * Kp * 2);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+    int64_t n = n_dst_max;
+    if (n_dst_dev) {
+        const int64_t m = *n_dst_dev;
+        n = m < n ? m : n;
+    }
+    const int64_t tiles = (n + kTileM - 1) / kTileM;
+    if ((int64_t)blockIdx.x >= tiles) return;   // whole CTA leaves before any TMEM / barrier use
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // --- setup: barrier, TMEM columns, W into shared memory -----------------------------------
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int c = threadIdx.x; c < N * (Kp >> 3); c += kThreads) {   // one 16 B chunk (8 k) per step
+        const int r = c / (Kp >> 3), k0 = (c % (Kp >> 3)) * 8;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = (k0 + e < dim) ? w[(int64_t)r * dim + k0 + e] : __float2bfloat16_rn(0.0f);
+        *reinterpret_cast<uint4*>(sB + core_off(r, k0, Kp)) = *reinterpret_cast<const uint4*>(v);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t bar_a = smem_u32(bar);
+    const uint32_t idesc = instr_desc(kTileM, N);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    uint32_t phase = 0;
+
+    for (int rep = 0; rep < repeat; ++rep) {
+        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            // --- 1. h for 128 rows -> bf16 A tile (warp per row, lane per 4 features) -----------
+            for (int rr = warp; rr < kTileM; rr += kWarps) {
+                const int64_t i = tile * kTileM + rr;
+                const bool live = i < n;
+                const int c = live ? cnt[i] : 0;
+                const float inv = 1.0f / (1.0f + (float)c);
+                const int32_t my_nbr = (live && lane < c && lane < fanout) ? nbr[i * fanout + lane] : 0;
+                // warp-uniform loops (c, Kp are uniform); lanes past dim only skip their loads
+                for (int kb = 0; kb < Kp; kb += 128) {
+                    const int k0 = kb + lane * 4;
+                    const bool on = live && k0 < dim;
+                    const bool vec = x_vec && on && k0 + 4 <= dim;
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                    const float* xi = x + i * (int64_t)dim + k0;
+                    if (vec) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(xi));
+                        a0 = v.x; a1 = v.y; a2 = v.z; a3 = v.w;
+                    } else if (on) {
+                        a0 = xi[0];
+                        if (k0 + 1 < dim) a1 = xi[1];
+                        if (k0 + 2 < dim) a2 = xi[2];
+                        if (k0 + 3 < dim) a3 = xi[3];
+                    }
+                    for (int q = 0; q < c; ++q) {
+                        const int32_t j = q < 32 ? __shfl_sync(0xffffffffu, my_nbr, q) : nbr[i * fanout + q];
+                        const float* xj = x + (int64_t)j * dim + k0;
+                        if (vec) {
+                            const float4 v = __ldg(reinterpret_cast<const float4*>(xj));
+                            a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+                        } else if (on) {
+                            a0 += xj[0];
+                            if (k0 + 1 < dim) a1 += xj[1];
+                            if (k0 + 2 < dim) a2 += xj[2];
+                            if (k0 + 3 < dim) a3 += xj[3];
+                        }
+                    }
+                    a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
+                    __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+                    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+                    if (k0 < Kp) *reinterpret_cast<uint2*>(sA + core_off(rr, k0, Kp)) = pk;
+                }
+            }
+            // generic-proxy stores -> visible to the tensor core (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            // --- 2. one thread issues the MMAs: D[tmem] = A . B^T over Kp / 16 steps -----------
+            if (threadIdx.x == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int s = 0; s < (Kp >> 4); ++s) {
+                    const uint64_t ad = smem_desc(a_base + s * 256, Kp), bd = smem_desc(b_base + s * 256, Kp);
+                    const uint32_t acc = s > 0;
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar_a)
+                             : "memory");
+            }
+            mbar_wait(bar_a, phase);
+            phase ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // --- 3. epilogue: TMEM -> registers -> y (lane = row, 8 columns per load) -----------
+            {
+                const int quarter = warp & 3, half = warp >> 2;
+                const int64_t row = tile * kTileM + quarter * 32 + lane;
+                const int c0 = half * (N >> 1), c1 = c0 + (N >> 1);
+                for (int col = c0; col < c1; col += 8) {
+                    uint32_t v[8];
+                    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col;
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                                   "=r"(v[7])
+                                 : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (row < n) {
+                        float4* dst = reinterpret_cast<float4*>(y + row * (int64_t)N + col);
+                        dst[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
+                                             __uint_as_float(v[3]));
+                        dst[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]),
+                                             __uint_as_float(v[7]));
+                    }
+                }
+            }
+            // TMEM reads done and A free before the next tile's writes / MMAs
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncthreads();
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+    }
+}
+
+}  // namespace
+
+using namespace dgz;
+
+extern "C" dgz_status dgz_sage_workspace(int64_t dim, int64_t hidden, int64_t* smem_bytes, int32_t* tmem_cols) {
+    DGZ_REQUIRE(dim >= 1 && hidden >= 1, "dgz_sage_workspace: dim and hidden must be >= 1");
+    const int64_t Kp = (dim + 15) / 16 * 16;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)hidden && cols < 512) cols <<= 1;
+    if (smem_bytes) *smem_bytes = (hidden + kTileM) * Kp * 2 + 16;
+    if (tmem_cols) *tmem_cols = (int32_t)cols;
+    return DGZ_OK;
+}
+
+extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const int32_t* nbr_local, const int32_t* cnt,
+                                           int32_t fanout, const int64_t* n_dst_dev, int64_t n_dst_max, const void* w_bf16,
+                                           int64_t hidden, float* y, int32_t repeat, int32_t sm_count, int32_t ctas_per_sm,
+                                           dgz_stream stream) {
+    DGZ_REQUIRE(x && nbr_local && cnt && w_bf16 && y && dim >= 1 && fanout >= 0 && n_dst_max >= 0 && repeat >= 1,
+                "dgz_sage_mean_linear: bad arguments");
+    DGZ_REQUIRE(hidden >= 16 && hidden <= 256 && hidden % 16 == 0,
+                "dgz_sage_mean_linear: hidden must be a multiple of 16 in [16, 256] (UMMA N with M = 128)");
+    DGZ_REQUIRE(((uintptr_t)y & 15) == 0, "dgz_sage_mean_linear: y must be 16-byte aligned");
+    DGZ_REQUIRE(((uintptr_t)w_bf16 & 1) == 0 && ((uintptr_t)x & 3) == 0, "dgz_sage_mean_linear: misaligned x or W");
+    if (n_dst_max == 0) return DGZ_OK;
+    int64_t need = 0;
+    int32_t cols = 0;
+    dgz_sage_workspace(dim, hidden, &need, &cols);
+    const int64_t Kp = (dim + 15) / 16 * 16;
+    DGZ_REQUIRE(need <= 227 * 1024, "dgz_sage_mean_linear: (hidden + 128) x dim bf16 operands exceed shared memory (%lld B)",
+                (long long)need);
+    // at most 512 / cols CTAs per SM may hold TMEM at once: size shared memory so no more fit
+    const int per_sm = 512 / cols;
+    int64_t smem = need;
+    const int64_t cap = (228 * 1024) / per_sm - 1024;
+    if (per_sm < 8 && smem < cap) smem = cap;
+    if (smem > 227 * 1024) smem = 227 * 1024;
+    DGZ_CUDA(cudaFuncSetAttribute(sage_mean_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nsm = sm_count_of_current_device();
+    const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
+    const int64_t tiles = (n_dst_max + kTileM - 1) / kTileM;
+    int64_t blocks = tiles;
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool x_vec = (dim % 4 == 0) && (((uintptr_t)x & 15) == 0);   // float4 row loads
+    const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(w_bf16);
+    if (ctas_per_sm > 0) {
+        const int64_t c = (int64_t)k * ctas_per_sm;
+        if (blocks > c) blocks = c;
+        sage_mean_linear_kernel<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout, n_dst_dev,
+                                                                     n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec);
+        dgz::count_launch();
+    } else {
+        for (int r = 0; r < repeat; ++r) {
+            sage_mean_linear_kernel<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout,
+                                                                         n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols,
+                                                                         y, 1, x_vec);
+            dgz::count_launch();
+        }
+    }
+    return launch_check("sage_mean_linear_kernel");
+}

@@ -130,6 +130,8 @@ _SIGS = {
     "dgz_sample_uniform": ([_P(Csr), _vp, _i64, _P(_i32), ctypes.c_int, _u64, _P(SampleOut), _vp], ctypes.c_int),
     "dgz_sample_check": ([_P(SampleOut), _vp], ctypes.c_int),
     "dgz_aggregate_mean": ([_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _i32, _i32, _i32, _vp], ctypes.c_int),
+    "dgz_sage_mean_linear": ([_vp, _i64, _vp, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _i32, _vp], ctypes.c_int),
+    "dgz_sage_workspace": ([_i64, _i64, _P(_i64), _P(_i32)], ctypes.c_int),
     "dgz_partition_create": ([_i32, _i32, _u32, _P(_vp)], ctypes.c_int),
     "dgz_partition_get": ([_vp, _P(_vp), _P(_vp), _P(_i32), _P(_i32)], ctypes.c_int),
     "dgz_partition_group_count": ([_P(_i32), _P(_i32)], ctypes.c_int),
@@ -667,6 +669,25 @@ def aggregate_mean(x: torch.Tensor, dim: int, nbr_local: torch.Tensor, cnt: torc
     _check(_lib.dgz_aggregate_mean(_dptr(x), dim, _dptr(nbr_local), _dptr(cnt), fanout, _dptr(n_dst_dev), n_dst_max,
                                    _dptr(y), repeat, sm_count, ctas_per_sm, _stream(stream)), "dgz_aggregate_mean")
     return y
+
+
+def sage_mean_linear(x: torch.Tensor, dim: int, nbr_local: torch.Tensor, cnt: torch.Tensor, fanout: int,
+                     n_dst_dev: torch.Tensor | None, n_dst_max: int, w: torch.Tensor, y: torch.Tensor, repeat: int = 1,
+                     sm_count: int = 0, ctas_per_sm: int = 0, stream=None) -> torch.Tensor:
+    """dgz_sage_mean_linear: y[:n_dst] = bf16(mean over self + sampled neighbours of x) @ w.T on the
+    tensor cores; w is bf16 [hidden, dim], y fp32 [>= n_dst, hidden]."""
+    assert w.dtype == torch.bfloat16 and w.dim() == 2 and w.shape[1] == dim, "w must be bf16 [hidden, dim]"
+    _check(_lib.dgz_sage_mean_linear(_dptr(x), dim, _dptr(nbr_local), _dptr(cnt), fanout, _dptr(n_dst_dev), n_dst_max,
+                                     _dptr(w), int(w.shape[0]), _dptr(y), repeat, sm_count, ctas_per_sm, _stream(stream)),
+           "dgz_sage_mean_linear")
+    return y
+
+
+def sage_workspace(dim: int, hidden: int) -> tuple:
+    """(shared-memory bytes, TMEM columns) of one dgz_sage_mean_linear CTA."""
+    b, c = _i64(), _i32()
+    _check(_lib.dgz_sage_workspace(dim, hidden, ctypes.byref(b), ctypes.byref(c)), "dgz_sage_workspace")
+    return b.value, c.value
 
 
 def probe_stream(src_dev_ptr: int, nbytes: int, sm_count: int, warps: int, unroll: int, sink: torch.Tensor, stream=None):

@@ -267,3 +267,46 @@ def test_merged_plan_sectors_brute_force():
             assert rm.merged_plan_sectors(ids, R, base) == want
             sparse = [i * 9 for i in range(50)]
             assert rm.merged_plan_sectors(sparse, R, base) == sum(rm.row_sectors(base + i * R, R) for i in sparse)
+
+
+# ----------------------------------------------------------------------------------------------
+# The consumer's layer: oracle.sage_mean_linear
+# ----------------------------------------------------------------------------------------------
+def _mat(s, conv=float):
+    return np.array([[conv(v) for v in row.split(",")] for row in s.split(";")])
+
+
+def test_sage_layer_worked_example():
+    """The hand-worked example in tests/golden/sage_layer_example.txt."""
+    from fractions import Fraction
+    g = dict(l.split(None, 1) for l in golden_lines("sage_layer_example.txt"))
+    x, w = _mat(g["x"]), _mat(g["w"])
+    local, cnt = _mat(g["local"], int), np.array([int(v) for v in g["cnt"].split(",")])
+    want = _mat(g["y"], lambda v: float(Fraction(v)))
+    got = oracle.sage_mean_linear(x, local, cnt, w)
+    assert np.allclose(got, want, rtol=0, atol=1e-15)
+
+
+def test_sage_layer_is_dense_normalised_adjacency_product():
+    """Y equals the paper's matrix form A_hat . H . W^T with A_hat built explicitly as a dense
+    [n_dst, n_src] matrix (self edge + one entry per sampled slot, repeated IDs adding up, rows
+    scaled by 1/(1+cnt)), on random blocks; and the two degenerate cases: no samples and W = I
+    give Y = H[:n_dst]; every row sampling itself f times with W = I gives Y = H[:n_dst]."""
+    rng = np.random.default_rng(11)
+    for n_src, n_dst, dim, hidden, f in ((40, 12, 5, 3, 4), (200, 64, 17, 32, 7), (9, 9, 1, 1, 3)):
+        x = rng.standard_normal((n_src, dim))
+        w = rng.standard_normal((hidden, dim))
+        cnt = rng.integers(0, f + 1, size=n_dst)
+        local = np.full((n_dst, f), -1, dtype=np.int64)
+        A = np.zeros((n_dst, n_src))
+        for i in range(n_dst):
+            local[i, :cnt[i]] = rng.integers(0, n_src, size=cnt[i])
+            A[i, i] += 1.0
+            for q in range(cnt[i]):
+                A[i, local[i, q]] += 1.0
+            A[i] /= 1.0 + cnt[i]
+        assert np.allclose(oracle.sage_mean_linear(x, local, cnt, w), A @ x @ w.T, rtol=1e-12, atol=1e-12)
+        eye = np.eye(dim)
+        assert np.array_equal(oracle.sage_mean_linear(x, local, np.zeros(n_dst, np.int64), eye), x[:n_dst])
+        selfs = np.repeat(np.arange(n_dst)[:, None], f, axis=1)
+        assert np.allclose(oracle.sage_mean_linear(x, selfs, np.full(n_dst, f), eye), x[:n_dst], rtol=1e-14, atol=1e-14)
