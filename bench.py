@@ -909,12 +909,24 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
     nstep = min(K, 8)
     ev2 = (ev(), ev())
 
+    hidden = args.consumer_hidden
+    # the layer needs its two bf16 operands in shared memory: wide rows (config 2, 602 fp32) take the mean
+    sage = args.consumer == "sage" and dgz.sage_workspace(dim, hidden)[0] <= 227 * 1024
+    # the layer's weight (nn.Linear layout [hidden, dim], bf16), seeded; only its shape matters for timing
+    w_layer = (torch.randn(hidden, dim, generator=torch.Generator().manual_seed(7)) / dim ** 0.5).to(torch.bfloat16).cuda()
+
     def consume(comp, mb, repeat, y, nb, cb):
-        dgz.aggregate_mean(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:], cfg.fanouts[L - 1],
-                           mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], y, repeat=repeat, stream=comp)
+        if sage:   # mean over the sampled neighbours, then the GEMM (tcgen05)
+            dgz.sage_mean_linear(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:],
+                                 cfg.fanouts[L - 1], mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], w_layer, y,
+                                 repeat=repeat, stream=comp)
+        else:
+            dgz.aggregate_mean(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:],
+                               cfg.fanouts[L - 1], mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], y, repeat=repeat,
+                               stream=comp)
 
     def measure(f, comp, repeat=None, t_target=None, timeline=False):
-        y = torch.empty((f.bufs[0].bounds[L - 1], dim), dtype=torch.float32, device="cuda")
+        y = torch.empty((f.bufs[0].bounds[L - 1], hidden if sage else dim), dtype=torch.float32, device="cuda")
         nb = sum(f.bufs[0].bounds[k] * cfg.fanouts[k] for k in range(L - 1))
         cb = sum(f.bufs[0].bounds[k] for k in range(L - 1))
         a, b = ev2
@@ -1074,7 +1086,9 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
             "hidden_frac_partitioned": hidden_partitioned,
             "hidden_frac_best_incl_fill": round(1 - max(0.0, best["t_step_overlapped_incl_fill_ms"] - t_c0) / t_g0, 3),
             "steps_measured": nstep, "sweep": rows, "timeline": timeline,
-            "consumer": "dgz_aggregate_mean over the last hop's block, non-persistent launches, repeated to T_c ~ T_fetch",
+            "consumer": (f"dgz_sage_mean_linear (mean over the sampled neighbours, then the {dim} x {hidden} bf16 GEMM on the "
+                         "tensor cores)" if sage else "dgz_aggregate_mean")
+                        + " over the last hop's block, non-persistent launches, repeated to T_c ~ T_fetch",
             "partition_gather": "candidate shapes (SMs, spread/contiguous, warps per SM) timed under load, 16 loads per "
                                 "lane, work-counter batches",
             "hidden": "hidden_frac_best = 1 - exposed / T_fetch for the shortest overlapped step, exposed = T_overlap - T_c "
@@ -1568,6 +1582,9 @@ def main():
     ap.add_argument("--dynamic", action="store_true", help="gather batches from a work counter (DGZ_GATHER_FLAG_DYNAMIC)")
     ap.add_argument("--overlap-warps", type=int, default=0,
                     help="warps per SM of every overlap candidate (0: each candidate's own)")
+    ap.add_argument("--consumer", default="sage", choices=["sage", "mean"],
+                    help="overlap leg's stand-in consumer: the GraphSAGE layer (mean + GEMM, a7) or the mean alone")
+    ap.add_argument("--consumer-hidden", type=int, default=256, help="the layer's output width (a multiple of 16, <= 256)")
     ap.add_argument("--timeline", default=None, help="write the overlap leg's best-shape timeline as a Chrome trace here")
     ap.add_argument("--oracle-budget", type=float, default=20.0, help="seconds of oracle work in the cpu_baseline leg")
     ap.add_argument("--no-baselines", action="store_true")

@@ -6,17 +6,20 @@
 //   y[i, :] = bf16(h[i, :]) . W^T            W: [hidden, dim] bf16 (nn.Linear layout), y fp32
 //
 // One CTA owns a tile of 128 destination nodes (the UMMA M):
-//   1. eight warps compute h for the tile from HBM (fp32, the same sequential order as
+//   1. sixteen warps compute h for the tile from HBM (fp32, the same sequential order as
 //      dgz_aggregate_mean, so h is bit-identical to it), round it to bf16 and write it into shared
 //      memory as the K-major A operand (core-matrix layout, SWIZZLE_NONE);
 //   2. one thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = hidden, K = 16 per
 //      instruction, fp32 accumulate) with A and W from shared memory and D in tensor memory, and
 //      commits to an mbarrier;
-//   3. the eight warps read D back with tcgen05.ld (warp w: TMEM lanes 32(w%4).., column half w/4)
+//   3. the sixteen warps read D back with tcgen05.ld (warp w: TMEM lanes 32(w%4).., 8-column chunks w/4 + 4c)
 //      and store y rows to HBM.
 // W is staged once per CTA in the same core-matrix layout (B operand, K-major).  The K dimension
-// is zero-padded to a multiple of 16.  Two CTAs share an SM (the TMEM columns and shared memory
-// are sized for it), so one CTA's MMA/epilogue overlaps the other's HBM-bound aggregation.
+// is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns, shared memory and the
+// 64-register budget are sized for it: 32 warps per SM keep the random row reads in flight), so one
+// CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
+// block (tools/consumer_roofline.py): 3.35 TB/s of algorithmic bytes, 0.51 of HBM (the mean alone,
+// dgz_aggregate_mean: 3.32 TB/s).
 #include "internal.h"
 
 #include <cuda_bf16.h>
@@ -24,7 +27,7 @@
 namespace {
 
 constexpr int kTileM = 128;
-constexpr int kThreads = 256;   // 8 warps
+constexpr int kThreads = 512;   // 16 warps
 constexpr int kWarps = kThreads / 32;
 
 // Core-matrix K-major layout of an [rows x Kp] bf16 operand (SWIZZLE_NONE, "interleave"):
@@ -62,11 +65,73 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
         : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+struct RowRef {
+    int64_t i;
+    int c;
+    float inv;
+    int32_t my_nbr;   // lane q holds the q-th sampled position (q < 32)
+    bool live;
+};
+
+__device__ __forceinline__ RowRef row_ref(int64_t i, int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ nbr,
+                                          int fanout, int lane) {
+    RowRef r;
+    r.i = i;
+    r.live = i < n;
+    // cnt and the nbr row are loaded independently (positions past cnt are never used)
+    r.c = r.live ? __ldg(cnt + i) : 0;
+    r.my_nbr = (r.live && lane < fanout) ? __ldg(nbr + i * fanout + lane) : 0;
+    r.inv = 1.0f / (1.0f + (float)r.c);
+    return r;
+}
+
+__device__ __forceinline__ uint2 pack_bf16(float4 s, float inv) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(s.x * inv, s.y * inv), hi = __floats2bfloat162_rn(s.z * inv, s.w * inv);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    return pk;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+
+// x[i] + sum_q x[nbr_q] at columns k0..k0+3 of one row (dim % 4 == 0, x 16 B aligned): the positions
+// of a batch are shuffled out first, then all its loads issue, then the adds run in q order.
+__device__ __forceinline__ float4 sum1_vec(const float* __restrict__ x, int dim, int k0, const RowRef& A,
+                                           const int32_t* __restrict__ nbr, int fanout) {
+    constexpr int kBatch = 8;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool on = A.live && k0 < dim;
+    float4 s = on ? ld4(x + A.i * (int64_t)dim + k0) : z;
+    for (int q0 = 0; q0 < A.c; q0 += kBatch) {
+        int32_t j[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+            const int qq = q0 + q;
+            j[q] = qq < 32 ? __shfl_sync(0xffffffffu, A.my_nbr, qq & 31) : (qq < A.c ? nbr[A.i * fanout + qq] : 0);
+        }
+        float4 v[kBatch];
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) v[q] = (on && q0 + q < A.c) ? ld4(x + (int64_t)j[q] * dim + k0) : z;
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q)
+            if (q0 + q < A.c) add4(s, v[q]);
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
 sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int32_t* __restrict__ nbr,
                         const int32_t* __restrict__ cnt, int fanout, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_max,
                         const __nv_bfloat16* __restrict__ w, int N, uint32_t tmem_cols, float* __restrict__ y, int repeat,
-                        bool x_vec) {
+                        bool x_vec, bool w_vec) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sB = smem;                                   // [N x Kp] bf16, core-matrix K-major
     uint8_t* sA = smem + (size_t)N * Kp * 2;              // [128 x Kp] bf16
@@ -95,10 +160,16 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
     }
     for (int c = threadIdx.x; c < N * (Kp >> 3); c += kThreads) {   // one 16 B chunk (8 k) per step
         const int r = c / (Kp >> 3), k0 = (c % (Kp >> 3)) * 8;
-        __align__(16) __nv_bfloat16 v[8];
+        uint4 pk;
+        if (w_vec && k0 + 8 <= dim) {
+            pk = __ldg(reinterpret_cast<const uint4*>(w + (int64_t)r * dim + k0));
+        } else {
+            __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = (k0 + e < dim) ? w[(int64_t)r * dim + k0 + e] : __float2bfloat16_rn(0.0f);
-        *reinterpret_cast<uint4*>(sB + core_off(r, k0, Kp)) = *reinterpret_cast<const uint4*>(v);
+            for (int e = 0; e < 8; ++e) v[e] = (k0 + e < dim) ? w[(int64_t)r * dim + k0 + e] : __float2bfloat16_rn(0.0f);
+            pk = *reinterpret_cast<const uint4*>(v);
+        }
+        *reinterpret_cast<uint4*>(sB + core_off(r, k0, Kp)) = pk;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -112,47 +183,43 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
     for (int rep = 0; rep < repeat; ++rep) {
         for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             // --- 1. h for 128 rows -> bf16 A tile (warp per row, lane per 4 features) -----------
-            for (int rr = warp; rr < kTileM; rr += kWarps) {
-                const int64_t i = tile * kTileM + rr;
-                const bool live = i < n;
-                const int c = live ? cnt[i] : 0;
-                const float inv = 1.0f / (1.0f + (float)c);
-                const int32_t my_nbr = (live && lane < c && lane < fanout) ? nbr[i * fanout + lane] : 0;
-                // warp-uniform loops (c, Kp are uniform); lanes past dim only skip their loads
-                for (int kb = 0; kb < Kp; kb += 128) {
-                    const int k0 = kb + lane * 4;
-                    const bool on = live && k0 < dim;
-                    const bool vec = x_vec && on && k0 + 4 <= dim;
-                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-                    const float* xi = x + i * (int64_t)dim + k0;
-                    if (vec) {
-                        const float4 v = __ldg(reinterpret_cast<const float4*>(xi));
-                        a0 = v.x; a1 = v.y; a2 = v.z; a3 = v.w;
-                    } else if (on) {
-                        a0 = xi[0];
-                        if (k0 + 1 < dim) a1 = xi[1];
-                        if (k0 + 2 < dim) a2 = xi[2];
-                        if (k0 + 3 < dim) a3 = xi[3];
+            if (x_vec) {
+                // one row per warp at a time, up to kBatch neighbour rows in flight (loads of a batch
+                // issued before its adds; the adds run in q order, so h stays bit-identical to
+                // dgz_aggregate_mean); the next row's count and positions load meanwhile
+                RowRef A = row_ref(tile * kTileM + warp, n, cnt, nbr, fanout, lane);
+                for (int rr = warp; rr < kTileM; rr += kWarps) {
+                    RowRef An = A;
+                    if (rr + kWarps < kTileM) An = row_ref(tile * kTileM + rr + kWarps, n, cnt, nbr, fanout, lane);
+                    for (int kb = 0; kb < Kp; kb += 128) {
+                        const int k0 = kb + lane * 4;
+                        const float4 sa = sum1_vec(x, dim, k0, A, nbr, fanout);
+                        if (k0 < Kp) *reinterpret_cast<uint2*>(sA + core_off(rr, k0, Kp)) = pack_bf16(sa, A.inv);
                     }
-                    for (int q = 0; q < c; ++q) {
-                        const int32_t j = q < 32 ? __shfl_sync(0xffffffffu, my_nbr, q) : nbr[i * fanout + q];
-                        const float* xj = x + (int64_t)j * dim + k0;
-                        if (vec) {
-                            const float4 v = __ldg(reinterpret_cast<const float4*>(xj));
-                            a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
-                        } else if (on) {
-                            a0 += xj[0];
-                            if (k0 + 1 < dim) a1 += xj[1];
-                            if (k0 + 2 < dim) a2 += xj[2];
-                            if (k0 + 3 < dim) a3 += xj[3];
+                    A = An;
+                }
+            } else {
+                for (int rr = warp; rr < kTileM; rr += kWarps) {   // scalar loads (dim % 4 != 0 or unaligned x)
+                    const RowRef A = row_ref(tile * kTileM + rr, n, cnt, nbr, fanout, lane);
+                    for (int kb = 0; kb < Kp; kb += 128) {
+                        const int k0 = kb + lane * 4;
+                        float v[4] = {0.f, 0.f, 0.f, 0.f};
+                        if (A.live) {
+                            const float* xi = x + A.i * (int64_t)dim;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (k0 + e < dim) v[e] = xi[k0 + e];
+                            for (int q = 0; q < A.c; ++q) {
+                                const int32_t j = q < 32 ? __shfl_sync(0xffffffffu, A.my_nbr, q) : nbr[A.i * fanout + q];
+                                const float* xj = x + (int64_t)j * dim;
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    if (k0 + e < dim) v[e] += xj[k0 + e];
+                            }
                         }
+                        if (k0 < Kp)
+                            *reinterpret_cast<uint2*>(sA + core_off(rr, k0, Kp)) = pack_bf16(make_float4(v[0], v[1], v[2], v[3]), A.inv);
                     }
-                    a0 *= inv; a1 *= inv; a2 *= inv; a3 *= inv;
-                    __nv_bfloat162 lo = __floats2bfloat162_rn(a0, a1), hi = __floats2bfloat162_rn(a2, a3);
-                    uint2 pk;
-                    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-                    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-                    if (k0 < Kp) *reinterpret_cast<uint2*>(sA + core_off(rr, k0, Kp)) = pk;
                 }
             }
             // generic-proxy stores -> visible to the tensor core (async proxy)
@@ -178,10 +245,9 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             // --- 3. epilogue: TMEM -> registers -> y (lane = row, 8 columns per load) -----------
             {
-                const int quarter = warp & 3, half = warp >> 2;
+                const int quarter = warp & 3, group = warp >> 2;   // TMEM lanes 32*quarter.. ; 8-column chunks
                 const int64_t row = tile * kTileM + quarter * 32 + lane;
-                const int c0 = half * (N >> 1), c1 = c0 + (N >> 1);
-                for (int col = c0; col < c1; col += 8) {
+                for (int col = group * 8; col < N; col += 8 * (kWarps / 4)) {
                     uint32_t v[8];
                     const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col;
                     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -253,18 +319,19 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
     int64_t blocks = tiles;
     cudaStream_t s = (cudaStream_t)stream;
     const bool x_vec = (dim % 4 == 0) && (((uintptr_t)x & 15) == 0);   // float4 row loads
+    const bool w_vec = (dim % 8 == 0) && (((uintptr_t)w_bf16 & 15) == 0);   // 16 B W loads
     const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(w_bf16);
     if (ctas_per_sm > 0) {
         const int64_t c = (int64_t)k * ctas_per_sm;
         if (blocks > c) blocks = c;
         sage_mean_linear_kernel<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout, n_dst_dev,
-                                                                     n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec);
+                                                                     n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec, w_vec);
         dgz::count_launch();
     } else {
         for (int r = 0; r < repeat; ++r) {
             sage_mean_linear_kernel<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout,
                                                                          n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols,
-                                                                         y, 1, x_vec);
+                                                                         y, 1, x_vec, w_vec);
             dgz::count_launch();
         }
     }
