@@ -18,8 +18,10 @@
 // is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns, shared memory and the
 // 64-register budget are sized for it: 32 warps per SM keep the random row reads in flight), so one
 // CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
-// block (tools/consumer_roofline.py): 3.35 TB/s of algorithmic bytes, 0.51 of HBM (the mean alone,
-// dgz_aggregate_mean: 3.32 TB/s).
+// block (tools/consumer_roofline.py): 3.75 TB/s of algorithmic bytes (0.57 of HBM) with one tile
+// per CTA, 4.06 TB/s (0.62) with two persistent CTAs per SM; the mean alone (dgz_aggregate_mean)
+// 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
+// chunks through the free A buffer so stores are 64 B row segments.
 #include "internal.h"
 
 #include <cuda_bf16.h>
@@ -161,8 +163,11 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
     for (int c = threadIdx.x; c < N * (Kp >> 3); c += kThreads) {   // one 16 B chunk (8 k) per step
         const int r = c / (Kp >> 3), k0 = (c % (Kp >> 3)) * 8;
         uint4 pk;
-        if (w_vec && k0 + 8 <= dim) {
-            pk = __ldg(reinterpret_cast<const uint4*>(w + (int64_t)r * dim + k0));
+        if (w_vec && k0 + 8 <= dim) {   // async copy: lands while the first tile's rows are summed
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sB + core_off(r, k0, Kp))),
+                         "l"(w + (int64_t)r * dim + k0)
+                         : "memory");
+            continue;
         } else {
             __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
@@ -171,10 +176,12 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
         }
         *reinterpret_cast<uint4*>(sB + core_off(r, k0, Kp)) = pk;
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    bool w_pending = true;
     const uint32_t bar_a = smem_u32(bar);
     const uint32_t idesc = instr_desc(kTileM, N);
     const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
@@ -222,6 +229,10 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
                     }
                 }
             }
+            if (w_pending) {   // this thread's W chunks have landed
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                w_pending = false;
+            }
             // generic-proxy stores -> visible to the tensor core (async proxy)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
@@ -243,9 +254,38 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
             mbar_wait(bar_a, phase);
             phase ^= 1;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            // --- 3. epilogue: TMEM -> registers -> y (lane = row, 8 columns per load) -----------
-            {
-                const int quarter = warp & 3, group = warp >> 2;   // TMEM lanes 32*quarter.. ; 8-column chunks
+            // --- 3. epilogue: TMEM -> registers -> y.  Warp w reads TMEM lanes 32(w%4).. (its rows)
+            if (Kp >= 128) {
+                // 16-column chunks staged through the (now free) A buffer, 2 KiB per warp, so each
+                // store instruction writes 8 rows x 64 contiguous bytes instead of 32 rows x 16 B
+                const int quarter = warp & 3, group = warp >> 2;
+                uint8_t* stage = sA + warp * 2048;
+                const int64_t row0 = tile * kTileM + quarter * 32;
+                for (int col = group * 16; col < N; col += 16 * (kWarps / 4)) {
+                    uint32_t v[16];
+                    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col;
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    const int sw = (lane >> 1) & 3;   // 16 B-chunk swizzle: conflict-free both ways
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        *reinterpret_cast<uint4*>(stage + lane * 64 + ((c ^ sw) * 16)) =
+                            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int it = 0; it < 4; ++it) {
+                        const int idx = it * 32 + lane, r = idx >> 2, c = idx & 3;
+                        const uint4 val = *reinterpret_cast<const uint4*>(stage + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
+                        if (row0 + r < n) *reinterpret_cast<uint4*>(y + (row0 + r) * (int64_t)N + col + c * 4) = val;
+                    }
+                    __syncwarp();
+                }
+            } else {
+                const int quarter = warp & 3, group = warp >> 2;   // direct: 8-column chunks
                 const int64_t row = tile * kTileM + quarter * 32 + lane;
                 for (int col = group * 8; col < N; col += 8 * (kWarps / 4)) {
                     uint32_t v[8];
