@@ -413,6 +413,10 @@ DGZ_API dgz_status dgz_partition_create_groups(const int32_t* fetch_groups, int3
 DGZ_API dgz_status dgz_partition_create(int32_t fetch_sms, int32_t fetch_priority, uint32_t flags, dgz_partition* out);
 DGZ_API dgz_status dgz_partition_get(dgz_partition p, dgz_stream* fetch_stream, dgz_stream* compute_stream,
                                      int32_t* fetch_sms, int32_t* compute_sms);
+/* Another non-blocking stream on group 0 (fetch) or 1 (compute) of the partition, e.g. so that the
+ * sampler of step j+1 runs on the fetch SMs beside the gather of step j (a5).  Owned by the
+ * partition: destroyed by dgz_partition_destroy. */
+DGZ_API dgz_status dgz_partition_stream(dgz_partition p, int32_t group, int32_t priority, dgz_stream* out);
 DGZ_API dgz_status dgz_partition_destroy(dgz_partition p);
 
 /* ==========================================================================================

@@ -63,6 +63,7 @@ struct dgz_partition_s {
     CUgreenCtx g[2] = {nullptr, nullptr};
     CUstream s[2] = {nullptr, nullptr};
     int sms[2] = {0, 0};
+    std::vector<CUstream> extra;   // dgz_partition_stream
 };
 
 using namespace dgz;
@@ -230,8 +231,19 @@ extern "C" dgz_status dgz_partition_get(dgz_partition p, dgz_stream* fetch_strea
     return DGZ_OK;
 }
 
+extern "C" dgz_status dgz_partition_stream(dgz_partition p, int32_t group, int32_t priority, dgz_stream* out) {
+    DGZ_REQUIRE(p && out && (group == 0 || group == 1), "dgz_partition_stream: bad arguments");
+    CUstream st = nullptr;
+    CUresult r = gdrv().stream_create(&st, p->g[group], CU_STREAM_NON_BLOCKING, priority);
+    if (r != CUDA_SUCCESS) return gfail(r, "cuGreenCtxStreamCreate");
+    p->extra.push_back(st);
+    *out = (dgz_stream)st;
+    return DGZ_OK;
+}
+
 extern "C" dgz_status dgz_partition_destroy(dgz_partition p) {
     DGZ_REQUIRE(p, "dgz_partition_destroy: null partition");
+    for (CUstream st : p->extra) gdrv().stream_destroy(st);
     for (int i = 0; i < 2; ++i) {
         if (p->s[i]) gdrv().stream_destroy(p->s[i]);
         if (p->g[i]) gdrv().destroy(p->g[i]);

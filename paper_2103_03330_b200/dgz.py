@@ -137,6 +137,7 @@ _SIGS = {
     "dgz_partition_group_count": ([_P(_i32), _P(_i32)], ctypes.c_int),
     "dgz_partition_create_groups": ([_P(_i32), _i32, _i32, _P(_vp)], ctypes.c_int),
     "dgz_partition_destroy": ([_vp], ctypes.c_int),
+    "dgz_partition_stream": ([_vp, _i32, _i32, _P(_vp)], ctypes.c_int),
     "dgz_probe_stream": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_probe_stream_hint": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
@@ -647,6 +648,12 @@ class Partition:
         self.fetch_sms, self.compute_sms = fn.value, cn.value
         self.fetch_stream = torch.cuda.ExternalStream(fs.value)
         self.compute_stream = torch.cuda.ExternalStream(cs.value)
+
+    def stream(self, group: int = 0, priority: int = 0):
+        """Another stream on the fetch (0) or compute (1) SMs, owned by the partition (dgz_partition_stream)."""
+        st = _vp()
+        _check(_lib.dgz_partition_stream(self.handle, group, priority, ctypes.byref(st)), "dgz_partition_stream")
+        return torch.cuda.ExternalStream(st.value)
 
     def destroy(self) -> None:
         if self.handle:

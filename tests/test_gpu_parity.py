@@ -365,7 +365,10 @@ def test_fetch_on_green_context_partition(dev):
             assert part.fetch_sms >= 8 and part.fetch_sms + part.compute_sms <= 148
             if groups is not None:
                 assert part.fetch_sms == len(groups) * per
-            f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, fetch_stream=part.fetch_stream)
+            # flags == 0 case: the sampler on a second stream of the fetch SMs (dgz_partition_stream), so sampling
+            # j+1 overlaps gathering j on the same partition
+            sstream = part.stream(0, -1) if (flags == 0 and groups is None) else None
+            f = MinibatchFetcher(t.table, g, c.fanouts, c.batch, fetch_stream=part.fetch_stream, sample_stream=sstream)
             for j in (0, 3):
                 seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
                 rs = gen.batch_rng_seed(c.seed, j)
