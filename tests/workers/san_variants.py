@@ -50,4 +50,13 @@ cnt = torch.full((500,), 5, dtype=torch.int32, device="cuda")
 y = torch.empty(500 * 64, dtype=torch.float32, device="cuda")
 dgz.aggregate_mean(x, 64, loc, cnt, 5, None, 500, y, repeat=2)
 torch.cuda.synchronize()
-print("bulk/segment/naive/shift/dynamic/cached/aggregate ok")
+# the a7 layer (tcgen05 MMA + TMEM): K 64 (direct epilogue) and K 128 (epilogue staged through shared memory)
+for d in (64, 128):
+    xs = torch.from_numpy(gen.float_table(2000 * d, 2)).cuda()
+    w = (torch.randn(256, d) / d ** 0.5).to(torch.bfloat16).cuda()
+    ys = torch.empty(500 * 256, dtype=torch.float32, device="cuda")
+    dgz.sage_mean_linear(xs, d, loc, cnt, 5, None, 500, w, ys, repeat=2)
+    dgz.sage_mean_linear(xs, d, loc, cnt, 5, None, 500, w, ys, ctas_per_sm=1, sm_count=2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(ys).all()
+print("bulk/segment/naive/shift/dynamic/cached/aggregate/sage ok")
