@@ -915,6 +915,8 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
     # the layer's weight (nn.Linear layout [hidden, dim], bf16), seeded; only its shape matters for timing
     w_layer = (torch.randn(hidden, dim, generator=torch.Generator().manual_seed(7)) / dim ** 0.5).to(torch.bfloat16).cuda()
 
+    cons_roof = {}
+
     def consume(comp, mb, repeat, y, nb, cb):
         if sage:   # mean over the sampled neighbours, then the GEMM (tcgen05)
             dgz.sage_mean_linear(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:],
@@ -950,11 +952,28 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
             b.record(comp)
             torch.cuda.synchronize()
             return a.elapsed_time(b) / nstep
-        if repeat is None:
+        calibrate = repeat is None
+        if calibrate:
             repeat = 8
             for _ in range(3):
                 repeat = max(1, int(round(repeat * (t_target or t_g) / cons_alone(repeat))))
         t_c = cons_alone(repeat)
+        if calibrate:   # the consumer kernel's own roofline: algorithmic HBM bytes per launch / launch time
+            n_dst = int(mb.sizes()[L - 1])
+            c = mb.bufs.cnt[cb:cb + n_dst].to(torch.int64).cpu()
+            f_last = cfg.fanouts[L - 1]
+            byts = (int(c.sum()) + n_dst) * dim * 4 + n_dst * (4 + 4 * f_last) + n_dst * (hidden if sage else dim) * 4
+            byts += hidden * dim * 2 if sage else 0
+            ms = t_c / repeat
+            peak = hbm_peak()
+            cons_roof.update({"kernel": "sage_mean_linear_kernel" if sage else "aggregate_mean_kernel", "bound": "hbm",
+                              "n_dst": n_dst, "launch_ms": round(ms, 4), "alg_bytes_per_launch": byts,
+                              "achieved_gbs": round(byts / ms / 1e6, 1), "peak_gbs": peak,
+                              "frac": round(byts / ms / 1e6 / peak, 3),
+                              "gemm_tflops": round(2.0 * n_dst * dim * hidden / ms / 1e9, 2) if sage else None,
+                              "how": "rows read (1 + cnt) x dim x 4 B + block (4 + 4 fanout) B + output row per dst node "
+                                     "(+ W once), per launch = T_c / repeat alone on the whole GPU; peak = "
+                                     "MEASURED_PEAKS.json hbm_gbs (else the guide's 6650)"})
         torch.cuda.synchronize()
         trace = []
         mbs = [f.fetch(seeds_dev[0], rng[0], timing=timeline)]
@@ -1092,7 +1111,8 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
         if args.timeline:
             write_chrome_trace(args.timeline, timeline)
     return {"t_fetch_ms": round(t_g0, 3), "consumer_repeat": repeat, "t_consumer_ms": round(t_c0, 3),
-            "t_consumer_samples_ms": [round(x, 3) for x in tcs], "serial_ms": round(t_g0 + t_c0, 3), "best": best,
+            "t_consumer_samples_ms": [round(x, 3) for x in tcs], "consumer_roofline": cons_roof,
+            "serial_ms": round(t_g0 + t_c0, 3), "best": best,
             "hidden_frac_best": round(1 - best["exposed_fetch_ms"] / t_g0, 3),
             "hidden_frac_partitioned": hidden_partitioned,
             "hidden_frac_best_incl_fill": round(1 - max(0.0, best["t_step_overlapped_incl_fill_ms"] - t_c0) / t_g0, 3),
