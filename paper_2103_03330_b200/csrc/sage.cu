@@ -15,9 +15,9 @@
 //   3. the sixteen warps read D back with tcgen05.ld (warp w: TMEM lanes 32(w%4).., 8-column chunks w/4 + 4c)
 //      and store y rows to HBM.
 // W is staged once per CTA in the same core-matrix layout (B operand, K-major).  The K dimension
-// is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns, shared memory and the
-// 64-register budget are sized for it: 32 warps per SM keep the random row reads in flight), so one
-// CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
+// is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns and a 56-register budget
+// are sized for it: 32 warps per SM keep the random row reads in flight, and a one-warp gather CTA
+// still fits beside them), so one CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
 // block (tools/consumer_roofline.py): 3.75 TB/s of algorithmic bytes (0.57 of HBM) with one tile
 // per CTA, 4.06 TB/s (0.62) with two persistent CTAs per SM; the mean alone (dgz_aggregate_mean)
 // 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
@@ -104,32 +104,46 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
     a.w += b.w;
 }
 
-// x[i] + sum_q x[nbr_q] at columns k0..k0+3 of one row (dim % 4 == 0, x 16 B aligned): the positions
-// of a batch are shuffled out first, then all its loads issue, then the adds run in q order.
-__device__ __forceinline__ float4 sum1_vec(const float* __restrict__ x, int dim, int k0, const RowRef& A,
-                                           const int32_t* __restrict__ nbr, int fanout) {
-    constexpr int kBatch = 8;
+// x[i] + sum_q x[nbr_q] at columns k0..k0+3 of NR rows at once (dim % 4 == 0, x 16 B aligned): the
+// positions of a batch of B neighbours per row are shuffled out first, then all the batch's loads
+// issue, then the adds run per row in q order.  Every guard is warp-uniform (cnt is per row).
+template <int NR, int B>
+__device__ __forceinline__ void sum_vec(const float* __restrict__ x, int dim, int k0, const RowRef (&A)[NR],
+                                        const int32_t* __restrict__ nbr, int fanout, float4 (&s)[NR]) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const bool on = A.live && k0 < dim;
-    float4 s = on ? ld4(x + A.i * (int64_t)dim + k0) : z;
-    for (int q0 = 0; q0 < A.c; q0 += kBatch) {
-        int32_t j[kBatch];
+    int cm = 0;
 #pragma unroll
-        for (int q = 0; q < kBatch; ++q) {
-            const int qq = q0 + q;
-            j[q] = qq < 32 ? __shfl_sync(0xffffffffu, A.my_nbr, qq & 31) : (qq < A.c ? nbr[A.i * fanout + qq] : 0);
-        }
-        float4 v[kBatch];
-#pragma unroll
-        for (int q = 0; q < kBatch; ++q) v[q] = (on && q0 + q < A.c) ? ld4(x + (int64_t)j[q] * dim + k0) : z;
-#pragma unroll
-        for (int q = 0; q < kBatch; ++q)
-            if (q0 + q < A.c) add4(s, v[q]);
+    for (int r = 0; r < NR; ++r) {
+        const bool on = A[r].live && k0 < dim;
+        s[r] = on ? ld4(x + A[r].i * (int64_t)dim + k0) : z;
+        cm = A[r].c > cm ? A[r].c : cm;
     }
-    return s;
+    for (int q0 = 0; q0 < cm; q0 += B) {
+        int32_t j[NR][B];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const int qq = q0 + q;
+                j[r][q] = 0;
+                if (qq < A[r].c) j[r][q] = qq < 32 ? __shfl_sync(0xffffffffu, A[r].my_nbr, qq & 31) : nbr[A[r].i * fanout + qq];
+            }
+        float4 v[NR][B];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                v[r][q] = (A[r].live && k0 < dim && q0 + q < A[r].c) ? ld4(x + (int64_t)j[r][q] * dim + k0) : z;
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (q0 + q < A[r].c) add4(s[r], v[r][q]);
+    }
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+template <int NR, int BATCH>
+__global__ void __maxnreg__(56)
 sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int32_t* __restrict__ nbr,
                         const int32_t* __restrict__ cnt, int fanout, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_max,
                         const __nv_bfloat16* __restrict__ w, int N, uint32_t tmem_cols, float* __restrict__ y, int repeat,
@@ -194,16 +208,30 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
                 // one row per warp at a time, up to kBatch neighbour rows in flight (loads of a batch
                 // issued before its adds; the adds run in q order, so h stays bit-identical to
                 // dgz_aggregate_mean); the next row's count and positions load meanwhile
-                RowRef A = row_ref(tile * kTileM + warp, n, cnt, nbr, fanout, lane);
-                for (int rr = warp; rr < kTileM; rr += kWarps) {
-                    RowRef An = A;
-                    if (rr + kWarps < kTileM) An = row_ref(tile * kTileM + rr + kWarps, n, cnt, nbr, fanout, lane);
+                RowRef A[NR];
+#pragma unroll
+                for (int r = 0; r < NR; ++r) A[r] = row_ref(tile * kTileM + warp + r * kWarps, n, cnt, nbr, fanout, lane);
+                for (int rr = warp; rr < kTileM; rr += NR * kWarps) {
+                    RowRef An[NR];
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) An[r] = A[r];
+                    if (rr + NR * kWarps < kTileM) {
+#pragma unroll
+                        for (int r = 0; r < NR; ++r)
+                            An[r] = row_ref(tile * kTileM + rr + (NR + r) * kWarps, n, cnt, nbr, fanout, lane);
+                    }
                     for (int kb = 0; kb < Kp; kb += 128) {
                         const int k0 = kb + lane * 4;
-                        const float4 sa = sum1_vec(x, dim, k0, A, nbr, fanout);
-                        if (k0 < Kp) *reinterpret_cast<uint2*>(sA + core_off(rr, k0, Kp)) = pack_bf16(sa, A.inv);
+                        float4 sa[NR];
+                        sum_vec<NR, BATCH>(x, dim, k0, A, nbr, fanout, sa);
+                        if (k0 < Kp) {
+#pragma unroll
+                            for (int r = 0; r < NR; ++r)
+                                *reinterpret_cast<uint2*>(sA + core_off(rr + r * kWarps, k0, Kp)) = pack_bf16(sa[r], A[r].inv);
+                        }
                     }
-                    A = An;
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) A[r] = An[r];
                 }
             } else {
                 for (int rr = warp; rr < kTileM; rr += kWarps) {   // scalar loads (dim % 4 != 0 or unaligned x)
@@ -346,13 +374,16 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
     const int64_t Kp = (dim + 15) / 16 * 16;
     DGZ_REQUIRE(need <= 227 * 1024, "dgz_sage_mean_linear: (hidden + 128) x dim bf16 operands exceed shared memory (%lld B)",
                 (long long)need);
-    // at most 512 / cols CTAs per SM may hold TMEM at once: size shared memory so no more fit
-    const int per_sm = 512 / cols;
-    int64_t smem = need;
-    const int64_t cap = (228 * 1024) / per_sm - 1024;
-    if (per_sm < 8 && smem < cap) smem = cap;
-    if (smem > 227 * 1024) smem = 227 * 1024;
-    DGZ_CUDA(cudaFuncSetAttribute(sage_mean_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // at most 512 / cols (>= 2) CTAs per SM may hold TMEM at once; the 56-register cap (2 x 512 x 56 of
+    // the 64 K registers) already limits the kernel to 2 CTAs per SM, and leaves room for one warp of a
+    // co-running gather (4 K registers) -- so shared memory is not padded: the gather's CTA fits beside two
+    // of these (2 x 97 KiB for dim 128 / hidden 256)
+    const int64_t smem = need;
+    // one row per warp at a time, neighbours loaded in batches of 6 (fanout <= 6: the whole row in one
+    // batch) or 8; measured on the config-4 last hop (fanout 5): 1 x 6 0.193 ms, 1 x 8 0.197, two rows per
+    // warp (2 x 4, 2 x 6) 0.209 / 0.238 -- they spill at the 64-register budget of 2 CTAs per SM
+    auto kern = fanout <= 6 ? sage_mean_linear_kernel<1, 6> : sage_mean_linear_kernel<1, 8>;
+    DGZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nsm = sm_count_of_current_device();
     const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
     const int64_t tiles = (n_dst_max + kTileM - 1) / kTileM;
@@ -364,12 +395,12 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
     if (ctas_per_sm > 0) {
         const int64_t c = (int64_t)k * ctas_per_sm;
         if (blocks > c) blocks = c;
-        sage_mean_linear_kernel<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout, n_dst_dev,
+        kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout, n_dst_dev,
                                                                      n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec, w_vec);
         dgz::count_launch();
     } else {
         for (int r = 0; r < repeat; ++r) {
-            sage_mean_linear_kernel<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout,
+            kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout,
                                                                          n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols,
                                                                          y, 1, x_vec, w_vec);
             dgz::count_launch();
