@@ -42,6 +42,7 @@ def lib() -> ctypes.CDLL:
         L.dgz_gen_cols32.argtypes = [i64, i64, u64, vp]
         L.dgz_gen_cols64.argtypes = [i64, i64, u64, vp]
         L.dgz_gen_fill.argtypes = [vp, i64, u64]
+        L.dgz_gen_fill_f32.argtypes = [vp, i64, u64]
         L.dgz_gen_batch_seeds.argtypes = [i64, i64, u64, i64, vp]
         L.dgz_gen_batch_seeds.restype = i64
         L.dgz_gen_batch_rng_seed.argtypes = [u64, i64]
@@ -109,6 +110,12 @@ def gen_csr_into(n: int, avg_degree: float, seed: int, alloc, skew_alpha: float 
 def fill_table(buf, nbytes: int, seed: int) -> None:
     """Fill ``nbytes`` bytes at ``buf`` (numpy array or raw address) with keyed random bits."""
     lib().dgz_gen_fill(_ptr(buf), int(nbytes), seed)
+
+
+def fill_table_f32(buf, count: int, seed: int) -> None:
+    """Fill ``count`` fp32 values at ``buf`` (numpy array or raw address) with finite keyed values in
+    [-1, 1) (multiples of 2^-23), in parallel."""
+    lib().dgz_gen_fill_f32(_ptr(buf), int(count), seed)
 
 
 def table_bytes(nbytes: int, seed: int) -> np.ndarray:

@@ -99,6 +99,15 @@ void dgz_gen_fill(uint8_t* p, int64_t nbytes, uint64_t seed) {
     }
 }
 
+/* count finite fp32 values, uniform on the 2^-23 grid of [-1, 1): value i = (top 24 bits of
+ * hk(seed, ST_TABLE + 100, i)) / 2^23 - 1, exact in fp32 (for consumers that do arithmetic on rows,
+ * at sizes numpy's generator is too slow for, e.g. the 56.9 GB config-4 table). */
+void dgz_gen_fill_f32(float* p, int64_t count, uint64_t seed) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < count; i++)
+        p[i] = (float)(hk(seed, ST_TABLE + 100, (uint64_t)i) >> 40) * (1.0f / 8388608.0f) - 1.0f;
+}
+
 /* Keyed bijection on [0, n) (6-round Feistel network on 2h bits with cycle walking). */
 static uint64_t feistel_perm(uint64_t x, uint64_t n, uint64_t key) {
     int bits = 2;

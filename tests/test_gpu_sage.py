@@ -158,3 +158,58 @@ def test_sage_layer_edges(dev):
         dgz.sage_mean_linear(big.view(-1), 320, loc.view(-1), cnt, f, None, 10, _weight(256, 320, 3),
                              torch.zeros(10, 256, device="cuda"))
     assert dgz.sage_workspace(128, 256) == ((256 + 128) * 128 * 2 + 16, 256)
+
+
+def test_sage_layer_full_size_config4(dev):
+    """BASELINE config 4 at full size, in the launch configuration bench.py times: the fetcher's GPU minibatch
+    (sampler + address-sorted zero-copy gather from the 56.9 GB table, here filled with finite fp32 values)
+    feeds the layer on the last hop's block (|F_2| ~ 1.5e5 destination rows, fanout 5, 128 -> 256,
+    non-persistent grid); 3000 random destination rows plus the first and last 64 are computed one by one
+    by the oracle from ITS sample and ITS gather of the rows they need."""
+    from paper_2103_03330_b200.pipeline import MinibatchFetcher
+    c = gen.CONFIGS[4]
+    dim, R, hidden = c.dim, c.row_bytes, 256
+    buf = dgz.HostBuffer(c.table_bytes + 4096, flags=dgz.HOST_HUGEPAGE)
+    gen.fill_table_f32(buf.ptr, c.n_nodes * dim, c.seed)
+    table = dgz.register_table(buf.ptr, c.n_nodes, dim, dgz.F32)
+    try:
+        off, col = gen.gen_csr(c.n_nodes, c.avg_degree, c.seed)
+        graph = dgz.Graph(torch.from_numpy(off).cuda(), torch.from_numpy(col).cuda())
+        f = MinibatchFetcher(table, graph, c.fanouts, c.batch)
+        j = 3
+        seeds = gen.batch_seeds(c.n_nodes, c.batch, c.seed, j)
+        rs = gen.batch_rng_seed(c.seed, j)
+        mb = f.fetch(torch.from_numpy(seeds).cuda(), rs)
+        sizes = mb.sizes()
+        L = len(c.fanouts)
+        k = L - 1
+        _, cnt_d, loc_d = mb.bufs.hop_blocks(sizes)[k]
+        nk = sizes[k]
+        w = _weight(hidden, dim, 44)
+        y = torch.full((mb.bufs.bounds[k], hidden), float("nan"), dtype=torch.float32, device="cuda")
+        dgz.sage_mean_linear(mb.rows.view(torch.float32).view(-1), dim, loc_d.reshape(-1), cnt_d, c.fanouts[k],
+                             mb.bufs.sizes_dev[k:k + 1], mb.bufs.bounds[k], w, y)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()
+        assert np.isnan(got[nk:]).all()
+        want = oracle.sample_uniform(off, col, seeds, c.fanouts, rs)
+        assert int(want.sizes[k]) == nk
+        rng = np.random.default_rng(5)
+        pick = np.unique(np.concatenate([rng.choice(nk, 3000, replace=False), np.arange(64), np.arange(nk - 64, nk)]))
+        loc, cnt = want.local[k][pick], want.cnt[k][pick]
+        # the rows these destinations read: themselves first (x_sub[i] = dst pick[i]), then their neighbours
+        nbr_pos = np.unique(np.concatenate([loc[i, :cnt[i]] for i in range(len(pick))]))
+        extra = np.setdiff1d(nbr_pos, pick)
+        pos = np.concatenate([pick, extra])
+        remap = {int(p): i for i, p in enumerate(pos)}
+        loc_sub = np.full_like(loc, -1)
+        for i in range(len(pick)):
+            loc_sub[i, :cnt[i]] = [remap[int(p)] for p in loc[i, :cnt[i]]]
+        host = buf.numpy(0, c.table_bytes)
+        xs = np.empty(len(pos) * R, dtype=np.uint8)
+        assert oracle.gather_into(host.ctypes.data, c.n_nodes, R, want.U[pos], xs) == 0
+        check_layer(got[pick], xs.view(np.float32).reshape(-1, dim), loc_sub, cnt, w)
+        dgz.check_errors(table)
+    finally:
+        table.unregister()
+        buf.free()

@@ -33,3 +33,18 @@ def test_rank_partition():
     owned = [gen.rank_batches(r, world, 5) for r in range(world)]
     flat = sorted(j for o in owned for j in o)
     assert flat == list(range(20)) and all(j % world == r for r, o in enumerate(owned) for j in o)
+
+
+def test_fill_table_f32():
+    """Finite keyed fp32 values on the 2^-23 grid of [-1, 1), deterministic in (seed, index), independent
+    of the count filled (keyed by position) -- the recipe of the layer's full-size parity table."""
+    a = np.empty(100_000, np.float32)
+    gen.fill_table_f32(a, a.size, 7)
+    assert np.isfinite(a).all() and a.min() >= -1.0 and a.max() < 1.0
+    assert np.array_equal(a * np.float32(2 ** 23), np.round(a * np.float32(2 ** 23)))
+    b = np.empty(1000, np.float32)
+    gen.fill_table_f32(b, b.size, 7)
+    assert np.array_equal(a[:1000], b)
+    gen.fill_table_f32(b, b.size, 8)
+    assert not np.array_equal(a[:1000], b)
+    assert abs(float(a.mean())) < 0.01 and abs(float(a.std()) - 3 ** -0.5) < 0.01
