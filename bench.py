@@ -921,7 +921,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
         if sage:   # mean over the sampled neighbours, then the GEMM (tcgen05)
             dgz.sage_mean_linear(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:],
                                  cfg.fanouts[L - 1], mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], w_layer, y,
-                                 repeat=repeat, stream=comp)
+                                 repeat=repeat, ctas_per_sm=args.consumer_ctas_per_sm, stream=comp)
         else:
             dgz.aggregate_mean(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:],
                                cfg.fanouts[L - 1], mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], y, repeat=repeat,
@@ -1616,6 +1616,8 @@ def main():
     ap.add_argument("--consumer", default="sage", choices=["sage", "mean"],
                     help="overlap leg's stand-in consumer: the GraphSAGE layer (mean + GEMM, a7) or the mean alone")
     ap.add_argument("--consumer-hidden", type=int, default=256, help="the layer's output width (a multiple of 16, <= 256)")
+    ap.add_argument("--consumer-ctas-per-sm", type=int, default=0,
+                    help="the layer as one persistent launch of this many CTAs per SM per step (0: `repeat` short launches)")
     ap.add_argument("--timeline", default=None, help="write the overlap leg's best-shape timeline as a Chrome trace here")
     ap.add_argument("--oracle-budget", type=float, default=20.0, help="seconds of oracle work in the cpu_baseline leg")
     ap.add_argument("--no-baselines", action="store_true")
