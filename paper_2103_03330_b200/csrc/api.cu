@@ -13,6 +13,7 @@
 #include <atomic>
 #include <mutex>
 #include <map>
+#include <vector>
 
 #include <sys/syscall.h>
 #include <unistd.h>
@@ -47,6 +48,26 @@ int sm_count_of_current_device() {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int carveout_pct() {
+    static const int pct = [] {
+        const char* e = getenv("DGZ_CARVEOUT");
+        return e ? atoi(e) : (int)cudaSharedmemCarveoutMaxShared;
+    }();
+    return pct;
+}
+
+void apply_carveout(const void* kernel) {
+    const int pct = carveout_pct();
+    if (pct < 0) return;
+    static std::mutex mu;
+    static std::vector<const void*> done;
+    std::lock_guard<std::mutex> lk(mu);
+    for (const void* k : done)
+        if (k == kernel) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    done.push_back(kernel);
+}
 
 static double now_s() {
     timespec ts;

@@ -335,6 +335,8 @@ inline int hints_of(int flags) {
 
 template <int SW, int U, bool MERGE, typename IdxT>
 void launch_segment_k(const dgz_table_s* t, const IdxT* idx, const SegLaunch& L) {
+    dgz::apply_carveout(L.cache ? (const void*)gather_segment_kernel<SW, U, MERGE, true, IdxT>
+                                : (const void*)gather_segment_kernel<SW, U, MERGE, false, IdxT>);
     if (L.cache) {
         gather_segment_kernel<SW, U, MERGE, true, IdxT><<<L.blocks, L.threads, 0, L.s>>>(
             t->dev, t->rows, t->row_bytes, idx, L.dst_pos, L.n, L.n_dev, L.out, L.err, L.blocked, *L.cache, hints_of(L.flags),
@@ -378,14 +380,17 @@ cudaError_t launch_elem(const dgz_table_s* t, const IdxT* idx, int64_t n, const 
                         cudaStream_t s) {
     switch (t->elem_bytes) {
         case 4:
+            dgz::apply_carveout((const void*)gather_elem_kernel<uint32_t, SHIFT, IdxT>);
             gather_elem_kernel<uint32_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint32_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
                                                                            (uint32_t*)out, err); dgz::count_launch();
             break;
         case 2:
+            dgz::apply_carveout((const void*)gather_elem_kernel<uint16_t, SHIFT, IdxT>);
             gather_elem_kernel<uint16_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint16_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
                                                                            (uint16_t*)out, err); dgz::count_launch();
             break;
         default:
+            dgz::apply_carveout((const void*)gather_elem_kernel<uint8_t, SHIFT, IdxT>);
             gather_elem_kernel<uint8_t, SHIFT, IdxT><<<blocks, 512, 0, s>>>((const uint8_t*)t->dev, t->rows, t->dim, idx, n, n_dev,
                                                                           (uint8_t*)out, err); dgz::count_launch();
     }

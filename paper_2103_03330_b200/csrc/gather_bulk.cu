@@ -157,6 +157,7 @@ cudaError_t launch_bulk(const dgz_table_s* t, const IdxT* idx, const int64_t* ds
     const size_t smem = (((size_t)S * 16 + 127) & ~size_t(127)) + (size_t)S * slot_bytes;
     cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<SW, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    dgz::apply_carveout((const void*)gather_bulk_kernel<SW, IdxT>);
     gather_bulk_kernel<SW, IdxT><<<blocks, threads, smem, s>>>(t->dev, t->rows, t->row_bytes, idx, dst_pos, n, n_dev, out, err, S,
                                                                slot_bytes, blocked); dgz::count_launch();
     return cudaGetLastError();

@@ -32,6 +32,15 @@ inline dgz_status launch_check(const char* what) {
 int sm_count_of_current_device();
 void count_launch();  // every kernel launch of libdgz increments dgz_kernel_launches()
 
+// Shared-memory carveout requested for the fetch-path kernels (cudaFuncAttributePreferredSharedMemoryCarveout,
+// set once per kernel): the maximum shared memory by default, DGZ_CARVEOUT=<percent> to change it, -1 to leave
+// it to the driver.  An SM runs CTAs of kernels whose carveouts differ only after it drains and reconfigures,
+// so a fetch kernel with the driver's small-smem carveout keeps a shared-memory-heavy consumer (the a7
+// layer: ~196 KiB per SM) off every SM it occupies (a one-warp spin kernel on 64 SMs
+// stretched the layer 1.46x with the driver's carveout, 1.01x with the maximum).
+int carveout_pct();
+void apply_carveout(const void* kernel);
+
 }  // namespace dgz
 
 struct dgz_table_s {

@@ -79,6 +79,7 @@ using namespace dgz;
 
 extern "C" dgz_status dgz_probe_spin(int32_t ctas, int32_t threads, int64_t iters, float* sink_dev, dgz_stream stream) {
     DGZ_REQUIRE(ctas > 0 && threads > 0 && threads <= 1024 && iters >= 0 && sink_dev, "dgz_probe_spin: bad args");
+    dgz::apply_carveout((const void*)spin_kernel);
     spin_kernel<<<ctas, threads, 0, (cudaStream_t)stream>>>(iters, sink_dev);
     dgz::count_launch();
     return launch_check("spin_kernel");

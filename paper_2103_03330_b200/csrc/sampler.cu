@@ -462,6 +462,12 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
 
     unsigned long long* status = (unsigned long long*)(ws + l.o_status);
     unsigned* tickets = (unsigned*)(ws + l.o_ticket);
+    for (const void* k : {(const void*)seeds_small_kernel, (const void*)seeds_mark_kernel, (const void*)seeds_min_kernel,
+                          (const void*)seeds_count_kernel, (const void*)scan_chunks_kernel, (const void*)seeds_emit_kernel,
+                          (const void*)posmap_range_kernel, (const void*)hop_sample_kernel<int64_t>,
+                          (const void*)hop_sample_kernel<int32_t>, (const void*)bitmap_compact_kernel<MODE_NEW>,
+                          (const void*)bitmap_compact_kernel<MODE_ALL>, (const void*)local_all_kernel})
+        dgz::apply_carveout(k);   // co-residency with shared-memory-heavy consumers (internal.h)
     DGZ_CUDA(cudaMemsetAsync(ws, 0, l.o_zero_end, s));  // error word, bitmaps, look-back state
     // F_0 (pos[] of every ID of U is written where the ID is emitted)
     if (n_seeds > 0 && n_seeds <= kSmallSeeds) {
