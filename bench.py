@@ -1038,6 +1038,8 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
             gpart, sstream = parts[0], None
             if where == "fetch partition, own stream":   # sampling j+1 beside gathering j on the same SMs
                 sstream = gpart.stream(0, -1)
+            elif where == "own stream":   # a high-priority stream of the primary context: the whole GPU, beside the consumer
+                sstream = torch.cuda.Stream(priority=-1)
         comp = gpart.compute_stream if cons == "partition" else comp0
         if where == "consumer stream":
             sstream = comp
@@ -1054,7 +1056,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
         combos = ((("fetch partition", "partition"), ("fetch partition, own stream", "partition"),
                    ("consumer stream", "partition")) if placement == "partition"
                   else (("fetch partition", "whole GPU"), ("fetch partition, own stream", "whole GPU"),
-                        ("consumer stream", "whole GPU"), ("own 8-SM partition", "whole GPU")))
+                        ("consumer stream", "whole GPU"), ("own stream", "whole GPU"), ("own 8-SM partition", "whole GPU")))
         for where, cons in combos:
             if where == "own 8-SM partition" and not spread:
                 continue
