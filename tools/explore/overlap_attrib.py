@@ -68,6 +68,9 @@ def main():
     out = torch.empty(828_000 * R, dtype=torch.uint8, device="cuda")
     gcfg = dgz.gather_cfg(sm_count=part.fetch_sms, warps_per_cta=a.warps, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
 
+    # round 2 also tried the BULK (TMA) gather with its ring capped at 24 KiB so it co-resides with the layer:
+    # no better (24 SMs: 1.18x vs 1.10x stretch), so that flag was not kept
+    bcfg = dgz.gather_cfg(variant=dgz.GATHER_BULK, sm_count=part.fetch_sms, warps_per_cta=4)
     prim = torch.cuda.Stream(priority=-1)   # primary context, high priority: a bounded grid, SMs chosen by the scheduler
 
     def corunner(kind, ms_target):
@@ -78,6 +81,9 @@ def main():
         elif kind == "gather_primary":
             for _ in range(int(ms_target / 8) + 1):
                 dgz.gather(table, ids, out, cfg=gcfg, stream=prim)
+        elif kind in ("bulk", "bulk_primary"):   # TMA bulk copies into the shared-memory ring
+            for _ in range(int(ms_target / 8) + 1):
+                dgz.gather(table, ids, out, cfg=bcfg, stream=prim if kind == "bulk_primary" else ps)
         elif kind == "spin":
             dgz.probe_spin(part.fetch_sms, 32 * a.warps, int(ms_target * 1.9e6 / 4), sink, stream=ps)
         elif kind == "pcie":
@@ -98,30 +104,32 @@ def main():
     for _ in range(2):
         run("none")
     base = float(np.median([run("none") for _ in range(3)]))
-    for st in (ps, prim):   # the gather alone, on the partition and as a bounded grid
+    dgz.gather(table, ids, out, cfg=gcfg, stream=ps)   # first touch of the managed table's GPU mapping
+    for st, c_, what in ((ps, gcfg, "segment, partition"), (prim, gcfg, "segment, bounded grid"),
+                         (ps, bcfg, "bulk small ring, partition"), (prim, bcfg, "bulk, bounded grid")):
         torch.cuda.synchronize()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(st)
         for _ in range(4):
-            dgz.gather(table, ids, out, cfg=gcfg, stream=st)
+            dgz.gather(table, ids, out, cfg=c_, stream=st)
         g1.record(st)
         torch.cuda.synchronize()
-        print(json.dumps({"gather_alone_ms": round(g0.elapsed_time(g1) / 4, 3),
-                          "where": "partition" if st is ps else "bounded grid, primary context"}), flush=True)
+        print(json.dumps({"gather_alone_ms": round(g0.elapsed_time(g1) / 4, 3), "where": what}), flush=True)
     print(json.dumps({"corunner": "none", "consumer_ms": round(base, 3), "sms": part.fetch_sms, "warps": a.warps}), flush=True)
     kinds = os.environ.get("ATTRIB_KINDS", "spin,pcie,gather,spin_primary,gather_primary").split(",")
     for kind in kinds:
         t = float(np.median([run(kind) for _ in range(3)]))
         # the co-runner's own time beside the consumer (gathers only): 8 gathers back to back under the consumer
         g_ms = None
-        if kind.startswith("gather"):
+        if kind.startswith("gather") or kind.startswith("bulk"):
             st = prim if kind.endswith("primary") else ps
+            c_ = bcfg if kind.startswith("bulk") else gcfg
             torch.cuda.synchronize()
             g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             dgz.sage_mean_linear(x.view(-1), dim, loc.view(-1), cnt, f, None, n_dst, w, y, repeat=a.repeat * 8, stream=comp)
             g0.record(st)
             for _ in range(4):
-                dgz.gather(table, ids, out, cfg=gcfg, stream=st)
+                dgz.gather(table, ids, out, cfg=c_, stream=st)
             g1.record(st)
             torch.cuda.synchronize()
             g_ms = round(g0.elapsed_time(g1) / 4, 3)
