@@ -918,6 +918,11 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
     cons_roof = {}
 
     def consume(comp, mb, repeat, y, nb, cb):
+        torch.cuda.nvtx.range_push("dgz.consume")
+        _consume(comp, mb, repeat, y, nb, cb)
+        torch.cuda.nvtx.range_pop()
+
+    def _consume(comp, mb, repeat, y, nb, cb):
         if sage:   # mean over the sampled neighbours, then the GEMM (tcgen05)
             dgz.sage_mean_linear(mb.rows.view(torch.float32).view(-1), dim, mb.bufs.local[nb:], mb.bufs.cnt[cb:],
                                  cfg.fanouts[L - 1], mb.bufs.sizes_dev[L - 1:L], mb.bufs.bounds[L - 1], w_layer, y,

@@ -148,6 +148,7 @@ class MinibatchFetcher:
         L = len(self.fanouts)
         if self.graphs and n_seeds == self.max_seeds:
             return self._fetch_graph(p, seeds, rng_seed, ev, count_into)
+        torch.cuda.nvtx.range_push(f"dgz.sample slot {p}")   # host-side ranges for nsys timelines
         with torch.cuda.stream(ss):
             if ev:
                 ev[0].record(ss)
@@ -158,7 +159,9 @@ class MinibatchFetcher:
                 b.rng_dev.fill_(_as_i64(rng_seed))
             dgz.sample_uniform(self.graph, seeds, self.fanouts, rng_seed, b, stream=ss)
             self.sampled[p].record(ss)
+        torch.cuda.nvtx.range_pop()
         gs.wait_event(self.sampled[p])
+        torch.cuda.nvtx.range_push(f"dgz.gather slot {p}")
         with torch.cuda.stream(gs):
             if ev:
                 ev[1].record(gs)
@@ -176,6 +179,7 @@ class MinibatchFetcher:
             if count_into is not None:
                 count_into.copy_(b.sizes_dev[L:L + 1], non_blocking=True)
             self.events[p].record(gs)
+        torch.cuda.nvtx.range_pop()
         return Minibatch(p, b, self.rows[p], self.events[p], self.fanouts, ev)
 
     # ---- CUDA-graph mode ----------------------------------------------------------------------
