@@ -49,16 +49,20 @@ int sm_count_of_current_device() {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int carveout_pct() {
-    static const int pct = [] {
+int carveout_pct(int cls) {
+    static const int gather_pct = [] {
         const char* e = getenv("DGZ_CARVEOUT");
         return e ? atoi(e) : (int)cudaSharedmemCarveoutMaxShared;
     }();
-    return pct;
+    static const int sampler_pct = [] {
+        const char* e = getenv("DGZ_SAMPLER_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    return cls == kCarveoutSampler ? sampler_pct : gather_pct;
 }
 
-void apply_carveout(const void* kernel) {
-    const int pct = carveout_pct();
+void apply_carveout(const void* kernel, int cls) {
+    const int pct = carveout_pct(cls);
     if (pct < 0) return;
     static std::mutex mu;
     static std::vector<const void*> done;

@@ -32,14 +32,18 @@ inline dgz_status launch_check(const char* what) {
 int sm_count_of_current_device();
 void count_launch();  // every kernel launch of libdgz increments dgz_kernel_launches()
 
-// Shared-memory carveout requested for the fetch-path kernels (cudaFuncAttributePreferredSharedMemoryCarveout,
-// set once per kernel): the maximum shared memory by default, DGZ_CARVEOUT=<percent> to change it, -1 to leave
-// it to the driver.  An SM runs CTAs of kernels whose carveouts differ only after it drains and reconfigures,
-// so a fetch kernel with the driver's small-smem carveout keeps a shared-memory-heavy consumer (the a7
+// Shared-memory carveout requested for a kernel (cudaFuncAttributePreferredSharedMemoryCarveout, set once per
+// kernel).  Gathers (kCarveoutGather): the maximum shared memory by default (DGZ_CARVEOUT=<percent> to change
+// it, -1 = the driver's choice).  An SM runs CTAs of kernels whose carveouts differ only after it drains and
+// reconfigures, so a gather with the driver's small-smem carveout keeps a shared-memory-heavy consumer (the a7
 // layer: ~196 KiB per SM) off every SM it occupies (a one-warp spin kernel on 64 SMs
-// stretched the layer 1.46x with the driver's carveout, 1.01x with the maximum).
-int carveout_pct();
-void apply_carveout(const void* kernel);
+// stretched the layer 1.46x with the driver's carveout, 1.01x with the maximum); the gathers' line loads
+// bypass L1, so the smaller L1 costs them nothing.  Sampler kernels (kCarveoutSampler): the driver's choice
+// by default (DGZ_SAMPLER_CARVEOUT to change it) -- their random CSR reads use L1 (maximum carveout: 0.29 ->
+// 0.34 ms per config-4 minibatch).
+constexpr int kCarveoutGather = 0, kCarveoutSampler = 1;
+int carveout_pct(int cls);
+void apply_carveout(const void* kernel, int cls = kCarveoutGather);
 
 }  // namespace dgz
 

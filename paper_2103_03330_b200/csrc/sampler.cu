@@ -467,7 +467,7 @@ extern "C" dgz_status dgz_sample_uniform(const dgz_csr* csr, const int64_t* seed
                           (const void*)posmap_range_kernel, (const void*)hop_sample_kernel<int64_t>,
                           (const void*)hop_sample_kernel<int32_t>, (const void*)bitmap_compact_kernel<MODE_NEW>,
                           (const void*)bitmap_compact_kernel<MODE_ALL>, (const void*)local_all_kernel})
-        dgz::apply_carveout(k);   // co-residency with shared-memory-heavy consumers (internal.h)
+        dgz::apply_carveout(k, dgz::kCarveoutSampler);   // internal.h
     DGZ_CUDA(cudaMemsetAsync(ws, 0, l.o_zero_end, s));  // error word, bitmaps, look-back state
     // F_0 (pos[] of every ID of U is written where the ID is emitted)
     if (n_seeds > 0 && n_seeds <= kSmallSeeds) {
