@@ -64,13 +64,15 @@ int carveout_pct(int cls) {
 void apply_carveout(const void* kernel, int cls) {
     const int pct = carveout_pct(cls);
     if (pct < 0) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
     static std::mutex mu;
-    static std::vector<const void*> done;
+    static std::vector<std::pair<const void*, int>> done;   // (kernel, device): the attribute is per device
     std::lock_guard<std::mutex> lk(mu);
-    for (const void* k : done)
-        if (k == kernel) return;
+    for (const auto& k : done)
+        if (k.first == kernel && k.second == dev) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    done.push_back(kernel);
+    done.emplace_back(kernel, dev);
 }
 
 static double now_s() {
