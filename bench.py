@@ -981,14 +981,15 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
                                      "MEASURED_PEAKS.json hbm_gbs (else the guide's 6650)"})
         torch.cuda.synchronize()
         trace = []
-        mbs = [f.fetch(seeds_dev[0], rng[0], timing=timeline)]
+        ahead = len(f.bufs) - 1   # minibatches fetched ahead of the one being consumed (slots - 1)
+        mbs = [f.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)], timing=timeline) for i in range(ahead)]
         a0 = ev()
         a0.record(comp)
         comp.wait_event(mbs[0].event)   # steady state: the pipeline's fill (the first fetch) is charged separately
         a.record(comp)
-        for i in range(1, nstep + 1):
+        for i in range(ahead, nstep + ahead):
             nxt = f.fetch(seeds_dev[i % len(rng)], rng[i % len(rng)], timing=timeline)
-            cur = mbs[-1]
+            cur = mbs.pop(0)
             comp.wait_event(cur.event)
             if timeline:
                 c0, c1 = ev(), ev()
@@ -999,7 +1000,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
                 trace.append((cur.timing, (c0, c1)))
             f.release(cur, comp)
             mbs.append(nxt)
-        comp.wait_event(mbs[-1].event)
+        comp.wait_event(mbs[0].event)   # the next minibatch is fetched too (as with 2 slots)
         b.record(comp)
         torch.cuda.synchronize()
         t_o = a.elapsed_time(b) / nstep
@@ -1050,7 +1051,7 @@ def run_overlap(dgz, fetcher, cfg, seeds_dev, rng, W, K, args):
             sstream = comp
         pcfg = dgz.gather_cfg(sm_count=gpart.fetch_sms, warps_per_cta=w, flags=dgz.FLAG_DEEP | dgz.FLAG_DYNAMIC)
         f = MinibatchFetcher(fetcher.table, fetcher.graph, cfg.fanouts, cfg.batch, fetch_stream=gpart.fetch_stream,
-                             gather_cfg=pcfg, sample_stream=sstream)
+                             gather_cfg=pcfg, sample_stream=sstream, slots=args.overlap_slots)
         return f, comp, parts, gpart
 
     for k, spread, w, placement in cands:
@@ -1623,6 +1624,8 @@ def main():
     ap.add_argument("--consumer", default="sage", choices=["sage", "mean"],
                     help="overlap leg's stand-in consumer: the GraphSAGE layer (mean + GEMM, a7) or the mean alone")
     ap.add_argument("--consumer-hidden", type=int, default=256, help="the layer's output width (a multiple of 16, <= 256)")
+    ap.add_argument("--overlap-slots", type=int, default=2,
+                    help="overlap leg: minibatch buffers in the ring (2 = ping-pong, P:546-561; 3 fetches two ahead)")
     ap.add_argument("--consumer-ctas-per-sm", type=int, default=0,
                     help="the layer as one persistent launch of this many CTAs per SM per step (0: `repeat` short launches)")
     ap.add_argument("--timeline", default=None, help="write the overlap leg's best-shape timeline as a Chrome trace here")
