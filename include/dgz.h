@@ -377,8 +377,9 @@ DGZ_API dgz_status dgz_aggregate_mean(const float* x, int64_t dim, const int32_t
  *   y[i, n] = sum_k bf16(h[i, k]) * w[n*dim + k]    fp32 accumulation on the tensor cores
  * x: fp32 [*, dim] device rows (the gathered minibatch), 4-byte aligned; w: bf16 [hidden, dim]
  * device, row-major (nn.Linear weight layout), 2-byte aligned; y: fp32 [n_dst, hidden] device,
- * 16-byte aligned, rows >= n_dst untouched.  hidden: a multiple of 16 in [16, 256]; (hidden + 128)
- * x ceil16(dim) x 2 bytes must fit in shared memory (dim 128 / hidden 256: 96 KiB).  h is rounded
+ * 16-byte aligned, rows >= n_dst untouched.  hidden: a multiple of 16 in [16, 256]; any dim (K is
+ * staged in chunks of up to (112 KiB / ((hidden + 128) x 2)) columns, accumulated in TMEM; dim 128 /
+ * hidden 256: one chunk, 96 KiB).  h is rounded
  * to bf16 (round to nearest even) before the product: |y - h.W^T| <= 2^-8 sum_k |h_k w_nk| plus
  * fp32 accumulation error.  repeat / sm_count / ctas_per_sm as for dgz_aggregate_mean.  Async on
  * `stream`; n_dst_max == 0 is a no-op.  Errors: DGZ_ERR_INVALID (arguments, sizes), DGZ_ERR_CUDA.
@@ -387,7 +388,7 @@ DGZ_API dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const int32
                               int32_t fanout, const int64_t* n_dst_dev, int64_t n_dst_max, const void* w_bf16,
                               int64_t hidden, float* y, int32_t repeat, int32_t sm_count, int32_t ctas_per_sm,
                               dgz_stream stream);
-/* Shared-memory bytes (the two bf16 operands) and TMEM columns one dgz_sage_mean_linear CTA uses. */
+/* Shared-memory bytes (one K chunk of both bf16 operands) and TMEM columns one dgz_sage_mean_linear CTA uses. */
 DGZ_API dgz_status dgz_sage_workspace(int64_t dim, int64_t hidden, int64_t* smem_bytes, int32_t* tmem_cols);
 
 /* ==========================================================================================

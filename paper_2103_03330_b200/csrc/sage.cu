@@ -144,14 +144,14 @@ __device__ __forceinline__ void sum_vec(const float* __restrict__ x, int dim, in
 
 template <int NR, int BATCH>
 __global__ void __maxnreg__(56)
-sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int32_t* __restrict__ nbr,
+sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk, const int32_t* __restrict__ nbr,
                         const int32_t* __restrict__ cnt, int fanout, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_max,
                         const __nv_bfloat16* __restrict__ w, int N, uint32_t tmem_cols, float* __restrict__ y, int repeat,
                         bool x_vec, bool w_vec) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sB = smem;                                   // [N x Kp] bf16, core-matrix K-major
-    uint8_t* sA = smem + (size_t)N * Kp * 2;              // [128 x Kp] bf16
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sA + (size_t)kTileM * Kp * 2);
+    uint8_t* sB = smem;                                   // [N x Kc] bf16, core-matrix K-major (one K chunk of W)
+    uint8_t* sA = smem + (size_t)N * Kc * 2;              // [128 x Kc] bf16 (the same K chunk of the means)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sA + (size_t)kTileM * Kc * 2);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
 
     int64_t n = n_dst_max;
@@ -174,28 +174,28 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
                      "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    for (int c = threadIdx.x; c < N * (Kp >> 3); c += kThreads) {   // one 16 B chunk (8 k) per step
-        const int r = c / (Kp >> 3), k0 = (c % (Kp >> 3)) * 8;
-        uint4 pk;
-        if (w_vec && k0 + 8 <= dim) {   // async copy: lands while the first tile's rows are summed
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sB + core_off(r, k0, Kp))),
-                         "l"(w + (int64_t)r * dim + k0)
-                         : "memory");
-            continue;
-        } else {
-            __align__(16) __nv_bfloat16 v[8];
+    // W's columns [kc0, kc0 + Kc) into sB: cp.async for whole 16 B pieces, zero padding past dim
+    auto load_w = [&](int kc0) {
+        for (int c = threadIdx.x; c < N * (Kc >> 3); c += kThreads) {   // one 16 B piece (8 k) per step
+            const int r = c / (Kc >> 3), kl = (c % (Kc >> 3)) * 8, kg = kc0 + kl;
+            if (w_vec && kg + 8 <= dim) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sB + core_off(r, kl, Kc))),
+                             "l"(w + (int64_t)r * dim + kg)
+                             : "memory");
+            } else {
+                __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = (k0 + e < dim) ? w[(int64_t)r * dim + k0 + e] : __float2bfloat16_rn(0.0f);
-            pk = *reinterpret_cast<const uint4*>(v);
+                for (int e = 0; e < 8; ++e) v[e] = (kg + e < dim) ? w[(int64_t)r * dim + kg + e] : __float2bfloat16_rn(0.0f);
+                *reinterpret_cast<uint4*>(sB + core_off(r, kl, Kc)) = *reinterpret_cast<const uint4*>(v);
+            }
         }
-        *reinterpret_cast<uint4*>(sB + core_off(r, k0, Kp)) = pk;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    bool w_pending = true;
+    bool w_resident = false;   // one chunk: W stays in shared memory for every tile of the CTA
     const uint32_t bar_a = smem_u32(bar);
     const uint32_t idesc = instr_desc(kTileM, N);
     const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
@@ -203,7 +203,11 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
 
     for (int rep = 0; rep < repeat; ++rep) {
         for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            // --- 1. h for 128 rows -> bf16 A tile (warp per row, lane per 4 features) -----------
+          for (int ci = 0; ci < nchunk; ++ci) {
+            const int kc0 = ci * Kc;
+            const bool load = !w_resident;   // W's chunk ci (every chunk, every tile, when K is chunked)
+            if (load) load_w(kc0);
+            // --- 1. h for 128 rows, columns [kc0, kc0 + Kc) -> bf16 A (warp per row, lane per 4 features)
             if (x_vec) {
                 // one row per warp at a time, up to kBatch neighbour rows in flight (loads of a batch
                 // issued before its adds; the adds run in q order, so h stays bit-identical to
@@ -220,14 +224,14 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
                         for (int r = 0; r < NR; ++r)
                             An[r] = row_ref(tile * kTileM + rr + (NR + r) * kWarps, n, cnt, nbr, fanout, lane);
                     }
-                    for (int kb = 0; kb < Kp; kb += 128) {
-                        const int k0 = kb + lane * 4;
+                    for (int kb = 0; kb < Kc; kb += 128) {
+                        const int kl = kb + lane * 4;
                         float4 sa[NR];
-                        sum_vec<NR, BATCH>(x, dim, k0, A, nbr, fanout, sa);
-                        if (k0 < Kp) {
+                        sum_vec<NR, BATCH>(x, dim, kc0 + kl, A, nbr, fanout, sa);
+                        if (kl < Kc) {
 #pragma unroll
                             for (int r = 0; r < NR; ++r)
-                                *reinterpret_cast<uint2*>(sA + core_off(rr + r * kWarps, k0, Kp)) = pack_bf16(sa[r], A[r].inv);
+                                *reinterpret_cast<uint2*>(sA + core_off(rr + r * kWarps, kl, Kc)) = pack_bf16(sa[r], A[r].inv);
                         }
                     }
 #pragma unroll
@@ -236,8 +240,8 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
             } else {
                 for (int rr = warp; rr < kTileM; rr += kWarps) {   // scalar loads (dim % 4 != 0 or unaligned x)
                     const RowRef A = row_ref(tile * kTileM + rr, n, cnt, nbr, fanout, lane);
-                    for (int kb = 0; kb < Kp; kb += 128) {
-                        const int k0 = kb + lane * 4;
+                    for (int kb = 0; kb < Kc; kb += 128) {
+                        const int kl = kb + lane * 4, k0 = kc0 + kl;
                         float v[4] = {0.f, 0.f, 0.f, 0.f};
                         if (A.live) {
                             const float* xi = x + A.i * (int64_t)dim;
@@ -252,24 +256,24 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
                                     if (k0 + e < dim) v[e] += xj[k0 + e];
                             }
                         }
-                        if (k0 < Kp)
-                            *reinterpret_cast<uint2*>(sA + core_off(rr, k0, Kp)) = pack_bf16(make_float4(v[0], v[1], v[2], v[3]), A.inv);
+                        if (kl < Kc)
+                            *reinterpret_cast<uint2*>(sA + core_off(rr, kl, Kc)) = pack_bf16(make_float4(v[0], v[1], v[2], v[3]), A.inv);
                     }
                 }
             }
-            if (w_pending) {   // this thread's W chunks have landed
+            if (load) {   // this thread's W pieces have landed
                 asm volatile("cp.async.wait_all;" ::: "memory");
-                w_pending = false;
+                w_resident = nchunk == 1;
             }
             // generic-proxy stores -> visible to the tensor core (async proxy)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
-            // --- 2. one thread issues the MMAs: D[tmem] = A . B^T over Kp / 16 steps -----------
+            // --- 2. one thread issues the MMAs: D[tmem] (+)= A . B^T over Kc / 16 steps ---------------
             if (threadIdx.x == 0) {
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (int s = 0; s < (Kp >> 4); ++s) {
-                    const uint64_t ad = smem_desc(a_base + s * 256, Kp), bd = smem_desc(b_base + s * 256, Kp);
-                    const uint32_t acc = s > 0;
+                for (int s = 0; s < (Kc >> 4); ++s) {
+                    const uint64_t ad = smem_desc(a_base + s * 256, Kc), bd = smem_desc(b_base + s * 256, Kc);
+                    const uint32_t acc = (ci > 0 || s > 0) ? 1u : 0u;
                     asm volatile(
                         "{\n\t.reg .pred p;\n\t"
                         "setp.ne.b32 p, %4, 0;\n\t"
@@ -279,11 +283,17 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar_a)
                              : "memory");
             }
+            // the MMAs have read A and B: both may be overwritten (next chunk) and D is complete (last chunk)
             mbar_wait(bar_a, phase);
             phase ^= 1;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (ci + 1 < nchunk) {
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncthreads();   // every warp past the wait before anyone rewrites A / B
+            }
+          }
             // --- 3. epilogue: TMEM -> registers -> y.  Warp w reads TMEM lanes 32(w%4).. (its rows)
-            if (Kp >= 128) {
+            if (Kc >= 128) {
                 // 16-column chunks staged through the (now free) A buffer, 2 KiB per warp, so each
                 // store instruction writes 8 rows x 64 contiguous bytes instead of 32 rows x 16 B
                 const int quarter = warp & 3, group = warp >> 2;
@@ -347,12 +357,21 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kp, const int3
 
 using namespace dgz;
 
+// K chunk of the operands in shared memory: all of K when (hidden + 128) x K bf16 fits the budget of two
+// CTAs per SM (112 KiB), else the largest multiple of 128 that does (>= 128 for hidden <= 256); the
+// kernel then accumulates the chunks in TMEM, re-staging W's chunk for every tile.
+static int64_t sage_chunk(int64_t dim, int64_t hidden) {
+    const int64_t Kp = (dim + 15) / 16 * 16, budget = 112 * 1024 - 16;
+    if ((hidden + kTileM) * Kp * 2 <= budget) return Kp;
+    int64_t kc = budget / ((hidden + kTileM) * 2) / 128 * 128;
+    return kc < 128 ? 128 : kc;
+}
+
 extern "C" dgz_status dgz_sage_workspace(int64_t dim, int64_t hidden, int64_t* smem_bytes, int32_t* tmem_cols) {
     DGZ_REQUIRE(dim >= 1 && hidden >= 1, "dgz_sage_workspace: dim and hidden must be >= 1");
-    const int64_t Kp = (dim + 15) / 16 * 16;
     uint32_t cols = 32;
     while (cols < (uint32_t)hidden && cols < 512) cols <<= 1;
-    if (smem_bytes) *smem_bytes = (hidden + kTileM) * Kp * 2 + 16;
+    if (smem_bytes) *smem_bytes = (hidden + kTileM) * sage_chunk(dim, hidden) * 2 + 16;
     if (tmem_cols) *tmem_cols = (int32_t)cols;
     return DGZ_OK;
 }
@@ -371,13 +390,12 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
     int64_t need = 0;
     int32_t cols = 0;
     dgz_sage_workspace(dim, hidden, &need, &cols);
-    const int64_t Kp = (dim + 15) / 16 * 16;
-    DGZ_REQUIRE(need <= 227 * 1024, "dgz_sage_mean_linear: (hidden + 128) x dim bf16 operands exceed shared memory (%lld B)",
-                (long long)need);
+    const int64_t Kp = (dim + 15) / 16 * 16, Kc = sage_chunk(dim, hidden), nchunk = (Kp + Kc - 1) / Kc;
+    DGZ_REQUIRE(dim < (int64_t(1) << 30), "dgz_sage_mean_linear: dim too large");
     // at most 512 / cols (>= 2) CTAs per SM may hold TMEM at once; the 56-register cap (2 x 512 x 56 of
     // the 64 K registers) already limits the kernel to 2 CTAs per SM, and leaves room for one warp of a
     // co-running gather (4 K registers) -- so shared memory is not padded: the gather's CTA fits beside two
-    // of these (2 x 97 KiB for dim 128 / hidden 256)
+    // of these (2 x 97 KiB for dim 128 / hidden 256; K is chunked to stay within that)
     const int64_t smem = need;
     // one row per warp at a time, neighbours loaded in batches of 6 (fanout <= 6: the whole row in one
     // batch) or 8; measured on the config-4 last hop (fanout 5): 1 x 6 0.193 ms, 1 x 8 0.197, two rows per
@@ -395,12 +413,12 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
     if (ctas_per_sm > 0) {
         const int64_t c = (int64_t)k * ctas_per_sm;
         if (blocks > c) blocks = c;
-        kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout, n_dst_dev,
+        kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kc, (int)nchunk, nbr_local, cnt, fanout, n_dst_dev,
                                                                      n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec, w_vec);
         dgz::count_launch();
     } else {
         for (int r = 0; r < repeat; ++r) {
-            kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kp, nbr_local, cnt, fanout,
+            kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kc, (int)nchunk, nbr_local, cnt, fanout,
                                                                          n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols,
                                                                          y, 1, x_vec, w_vec);
             dgz::count_launch();

@@ -111,6 +111,10 @@ def test_sage_layer_on_sampled_minibatch(dev, n_nodes, deg, dim, hidden, fanouts
     (64, 128, 10, 127),             # one short tile
     (16, 32, 2, 1000),
     (1, 16, 4, 300),                # dim 1: K padded 1 -> 16
+    (602, 256, 25, 300),            # config-2 rows (602 fp32): K in 5 chunks of 128 accumulated in TMEM
+    (320, 256, 5, 200),             # 3 chunks, the last one half padding
+    (300, 64, 10, 257),             # hidden 64: chunks of 256 (the second mostly padding)
+    (130, 48, 6, 400),              # dim 130: scalar loads (dim % 4 != 0), K 144 in one chunk
 ])
 def test_sage_layer_shapes(dev, dim, hidden, fanout, n_dst):
     """Synthetic blocks (random positions, counts 0..fanout, repeated IDs allowed) over every tile
@@ -132,7 +136,8 @@ def test_sage_layer_shapes(dev, dim, hidden, fanout, n_dst):
 
 def test_sage_layer_edges(dev):
     """n_dst = 0 is a no-op; a device count below the host bound leaves the rows past it untouched;
-    hidden outside {16, 32, ..., 256} and operands past shared memory are refused (DGZ_ERR_INVALID)."""
+    hidden outside {16, 32, ..., 256} is refused (DGZ_ERR_INVALID); rows too wide for one shared-memory
+    operand are chunked along K."""
     dim, hidden, f = 64, 32, 4
     x = torch.rand(500, dim, device="cuda")
     loc = torch.zeros(400, f, dtype=torch.int32, device="cuda")
@@ -153,11 +158,16 @@ def test_sage_layer_edges(dev):
         with pytest.raises(dgz.DgzError):
             dgz.sage_mean_linear(x.view(-1), dim, loc.view(-1), cnt, f, None, 400, _weight(bad_hidden, dim, 2),
                                  torch.zeros(400, bad_hidden, device="cuda"))
+    # wide rows are chunked along K (2 x 128 + a padded 64 here), not refused
     big = torch.rand(10, 320, device="cuda")
-    with pytest.raises(dgz.DgzError):     # (256 + 128) x 320 x 2 B > 227 KiB
-        dgz.sage_mean_linear(big.view(-1), 320, loc.view(-1), cnt, f, None, 10, _weight(256, 320, 3),
-                             torch.zeros(10, 256, device="cuda"))
+    yb = torch.zeros(10, 256, device="cuda")
+    wb = _weight(256, 320, 3)
+    dgz.sage_mean_linear(big.view(-1), 320, loc.view(-1), cnt, f, None, 10, wb, yb)
+    torch.cuda.synchronize()
+    check_layer(yb.cpu().numpy(), big.cpu().numpy(), loc[:10].cpu().numpy(), cnt[:10].cpu().numpy(), wb)
     assert dgz.sage_workspace(128, 256) == ((256 + 128) * 128 * 2 + 16, 256)
+    assert dgz.sage_workspace(602, 256) == ((256 + 128) * 128 * 2 + 16, 256)     # K chunk 128
+    assert dgz.sage_workspace(200, 64) == ((64 + 128) * 208 * 2 + 16, 64)        # one chunk
 
 
 def test_sage_layer_full_size_config4(dev):
