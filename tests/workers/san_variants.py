@@ -51,7 +51,7 @@ y = torch.empty(500 * 64, dtype=torch.float32, device="cuda")
 dgz.aggregate_mean(x, 64, loc, cnt, 5, None, 500, y, repeat=2)
 torch.cuda.synchronize()
 # the a7 layer (tcgen05 MMA + TMEM): K 64 (direct epilogue) and K 128 (epilogue staged through shared memory)
-for d in (64, 128):
+for d in (64, 128, 320):   # 320: K in three chunks
     xs = torch.from_numpy(gen.float_table(2000 * d, 2)).cuda()
     w = (torch.randn(256, d) / d ** 0.5).to(torch.bfloat16).cuda()
     ys = torch.empty(500 * 256, dtype=torch.float32, device="cuda")
