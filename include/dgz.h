@@ -439,6 +439,12 @@ DGZ_API dgz_status dgz_probe_stream(const void* src_dev, int64_t bytes, int32_t 
  * `iters` iterations.  Used to separate SM-issue from memory-system interference in the overlap
  * experiments.  sink_dev: device float [1]. */
 DGZ_API dgz_status dgz_probe_spin(int32_t ctas, int32_t threads, int64_t iters, float* sink_dev, dgz_stream stream);
+/* Random-row read probe (the a7 layer's access pattern): reads rows ids_dev[0..n) of row_bytes bytes
+ * (a multiple of 16) from the device-accessible src_dev, rows_in_flight (1, 2, 4, 8, 16) rows per warp
+ * issued before any is consumed, on sm_count SMs x warps warps; writes nothing but a sink word.  For
+ * the HBM ceiling of random row reads. */
+DGZ_API dgz_status dgz_probe_rows(const void* src_dev, int64_t row_bytes, const int64_t* ids_dev, int64_t n, int32_t sm_count,
+                                  int32_t warps, int32_t rows_in_flight, uint64_t* sink_dev, dgz_stream stream);
 DGZ_API dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream);
 
 #ifdef __cplusplus

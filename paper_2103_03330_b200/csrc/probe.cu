@@ -50,6 +50,31 @@ __global__ void __launch_bounds__(1024, 1) stream_kernel(const uint8_t* __restri
     if (acc == 0x9E3779B9u) atomicAdd((unsigned long long*)sink, 1ull);  // keeps the loads live
 }
 
+// random-row read probe: each warp reads U rows of R bytes (16 B per lane per step) at the given IDs
+// with all U rows' loads issued before any is consumed; XOR-folded, nothing written -- the read-only
+// ceiling of random row traffic (the a7 layer's pattern) at a given number of rows in flight
+template <int U>
+__global__ void __launch_bounds__(1024) rows_kernel(const uint8_t* __restrict__ src, int64_t R, const int64_t* __restrict__ ids,
+                                                    int64_t n, uint64_t* sink) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    uint32_t acc = 0;
+    for (int64_t r0 = w * U; r0 < n; r0 += nw * U) {
+        for (int64_t b = (int64_t)lane * 16; b < R; b += 512) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t r = r0 + u;
+                v[u] = r < n ? __ldg(reinterpret_cast<const uint4*>(src + __ldg(ids + r) * R + b)) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+        }
+    }
+    if (acc == 0x9E3779B9u) atomicAdd((unsigned long long*)sink, 1ull);
+}
+
 __global__ void chase_kernel(const int64_t* __restrict__ src, int64_t steps, uint64_t* cycles) {
     int64_t p = 0;
     const long long t0 = clock64();
@@ -120,6 +145,26 @@ extern "C" dgz_status dgz_probe_stream_hint(const void* src_dev, int64_t bytes, 
     }
     dgz::count_launch();
     return launch_check("stream_kernel (hint)");
+}
+
+extern "C" dgz_status dgz_probe_rows(const void* src_dev, int64_t row_bytes, const int64_t* ids_dev, int64_t n, int32_t sm_count,
+                                     int32_t warps, int32_t rows_in_flight, uint64_t* sink_dev, dgz_stream stream) {
+    DGZ_REQUIRE(src_dev && ids_dev && sink_dev && n > 0 && row_bytes > 0 && row_bytes % 16 == 0 && ((uintptr_t)src_dev % 16) == 0,
+                "dgz_probe_rows: bad args");
+    const int nsm = sm_count_of_current_device();
+    const int k = (sm_count > 0 && sm_count < nsm) ? sm_count : nsm;
+    if (warps <= 0 || warps > 32) warps = 32;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint8_t* src = (const uint8_t*)src_dev;
+    switch (rows_in_flight) {
+        case 1: rows_kernel<1><<<k, warps * 32, 0, s>>>(src, row_bytes, ids_dev, n, sink_dev); break;
+        case 2: rows_kernel<2><<<k, warps * 32, 0, s>>>(src, row_bytes, ids_dev, n, sink_dev); break;
+        case 4: rows_kernel<4><<<k, warps * 32, 0, s>>>(src, row_bytes, ids_dev, n, sink_dev); break;
+        case 16: rows_kernel<16><<<k, warps * 32, 0, s>>>(src, row_bytes, ids_dev, n, sink_dev); break;
+        default: rows_kernel<8><<<k, warps * 32, 0, s>>>(src, row_bytes, ids_dev, n, sink_dev); break;
+    }
+    dgz::count_launch();
+    return launch_check("rows_kernel");
 }
 
 extern "C" dgz_status dgz_probe_chase(const void* src_dev, int64_t steps, uint64_t* cycles_dev, dgz_stream stream) {

@@ -142,6 +142,7 @@ _SIGS = {
     "dgz_probe_chase": ([_vp, _i64, _vp, _vp], ctypes.c_int),
     "dgz_probe_stream_hint": ([_vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "dgz_probe_spin": ([_i32, _i32, _i64, _vp, _vp], ctypes.c_int),
+    "dgz_probe_rows": ([_vp, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -710,6 +711,13 @@ def probe_stream_hint(src_dev_ptr: int, nbytes: int, sm_count: int, warps: int, 
 
 def probe_chase(src_dev_ptr: int, steps: int, cycles: torch.Tensor, stream=None):
     _check(_lib.dgz_probe_chase(src_dev_ptr, steps, _dptr(cycles), _stream(stream)), "dgz_probe_chase")
+
+
+def probe_rows(src_dev_ptr: int, row_bytes: int, ids: torch.Tensor, sm_count: int, warps: int, rows_in_flight: int,
+               sink: torch.Tensor, stream=None):
+    """dgz_probe_rows: read the rows ids of src (row_bytes each), nothing written (random-row read ceiling)."""
+    _check(_lib.dgz_probe_rows(src_dev_ptr, row_bytes, _dptr(ids), ids.numel(), sm_count, warps, rows_in_flight, _dptr(sink),
+                               _stream(stream)), "dgz_probe_rows")
 
 
 def probe_spin(ctas: int, threads: int, iters: int, sink: torch.Tensor, stream=None):

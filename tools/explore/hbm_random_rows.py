@@ -35,6 +35,22 @@ def main():
     rng = np.random.default_rng(1)
     ids = rng.integers(0, a.rows, size=a.n).astype(np.int64)
     out = torch.empty(a.n * R, dtype=torch.uint8, device="cuda")
+    # read-only: the random-row read ceiling at several depths and warp counts (dgz_probe_rows)
+    sink = torch.zeros(4, dtype=torch.int64, device="cuda")
+    d = torch.from_numpy(ids).cuda()
+    for warps in (8, 16, 32):
+        for u in (1, 2, 4, 8, 16):
+            for _ in range(2):
+                dgz.probe_rows(tab.data_ptr(), R, d, 0, warps, u, sink)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                dgz.probe_rows(tab.data_ptr(), R, d, 0, warps, u, sink)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 5
+            print(json.dumps({"read_only": True, "warps_per_sm": warps, "rows_in_flight_per_warp": u, "n": a.n, "row_bytes": R,
+                              "ms": round(ms, 4), "read_gbs": round(a.n * R / ms / 1e6, 1)}), flush=True)
     for name, idx in (("random", ids), ("sorted", np.sort(ids))):
         d = torch.from_numpy(idx).cuda()
         for _ in range(3):
