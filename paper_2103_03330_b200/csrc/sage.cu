@@ -18,13 +18,16 @@
 // is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns and a 56-register budget
 // are sized for it: 32 warps per SM keep the random row reads in flight, and a one-warp gather CTA
 // still fits beside them), so one CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
-// block (tools/consumer_roofline.py): 3.75 TB/s of algorithmic bytes (0.57 of HBM) with one tile
-// per CTA, 4.06 TB/s (0.62) with two persistent CTAs per SM; the mean alone (dgz_aggregate_mean)
-// 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
+// block (tools/consumer_roofline.py): 4.11 TB/s of algorithmic bytes (0.63 of HBM) with the dynamic
+// tile schedule (3.75 TB/s with one tile per CTA); the mean alone (dgz_aggregate_mean) 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
 // chunks through the free A buffer so stores are 64 B row segments.
 #include "internal.h"
 
 #include <cuda_bf16.h>
+#include <stdlib.h>
+
+#include <atomic>
+#include <mutex>
 
 namespace {
 
@@ -147,12 +150,14 @@ __global__ void __maxnreg__(56)
 sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk, const int32_t* __restrict__ nbr,
                         const int32_t* __restrict__ cnt, int fanout, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_max,
                         const __nv_bfloat16* __restrict__ w, int N, uint32_t tmem_cols, float* __restrict__ y, int repeat,
-                        bool x_vec, bool w_vec) {
+                        bool x_vec, bool w_vec, unsigned long long* __restrict__ sched) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sB = smem;                                   // [N x Kc] bf16, core-matrix K-major (one K chunk of W)
     uint8_t* sA = smem + (size_t)N * Kc * 2;              // [128 x Kc] bf16 (the same K chunk of the means)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sA + (size_t)kTileM * Kc * 2);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+    int64_t* s_start = reinterpret_cast<int64_t*>(bar + 2);    // dynamic schedule: the grabbed rows' start
+    int32_t* s_rows = reinterpret_cast<int32_t*>(bar + 3);     // ... their count, and the first grab's size
 
     int64_t n = n_dst_max;
     if (n_dst_dev) {
@@ -160,7 +165,26 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
         n = m < n ? m : n;
     }
     const int64_t tiles = (n + kTileM - 1) / kTileM;
-    if ((int64_t)blockIdx.x >= tiles) return;   // whole CTA leaves before any TMEM / barrier use
+    // Dynamic schedule (sched != nullptr): CTAs grab row ranges from a counter, 128 rows at a time,
+    // except that the second CTA to arrive on an SM starts with 64 -- that puts the two CTAs of an SM
+    // half a mean phase apart, so one's MMA + epilogue runs while the other loads rows (in step, the
+    // phases added up: DESIGN.md section 4).  The first grab happens before any setup, so a CTA that
+    // finds no rows left leaves at once.
+    int64_t it_static = 0;
+    if (sched) {
+        if (threadIdx.x == 0) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            const unsigned long long slot = atomicAdd(sched + 1 + (smid & 255), 1ull);
+            const int want = (slot & 1) ? kTileM / 2 : kTileM;
+            *s_start = (int64_t)atomicAdd(sched, (unsigned long long)want);
+            *s_rows = want;
+        }
+        __syncthreads();
+        if (*s_start >= n) return;
+    } else if ((int64_t)blockIdx.x >= tiles) {
+        return;   // whole CTA leaves before any TMEM / barrier use
+    }
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -201,8 +225,27 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
     const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
     uint32_t phase = 0;
 
+    bool grabbed = sched != nullptr;   // the first range is already in s_start / s_rows
     for (int rep = 0; rep < repeat; ++rep) {
-        for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        it_static = 0;
+        while (true) {
+          int64_t r0, lim;   // rows [r0, lim) of this tile
+          if (sched) {
+              if (!grabbed) {
+                  if (threadIdx.x == 0) *s_start = (int64_t)atomicAdd(sched, (unsigned long long)kTileM), *s_rows = kTileM;
+                  __syncthreads();
+              }
+              grabbed = false;
+              r0 = *s_start;
+              if (r0 >= n) break;
+              lim = r0 + *s_rows < n ? r0 + *s_rows : n;
+          } else {
+              const int64_t tile = blockIdx.x + it_static * gridDim.x;
+              ++it_static;
+              if (tile >= tiles) break;
+              r0 = tile * kTileM;
+              lim = r0 + kTileM < n ? r0 + kTileM : n;
+          }
           for (int ci = 0; ci < nchunk; ++ci) {
             const int kc0 = ci * Kc;
             const bool load = !w_resident;   // W's chunk ci (every chunk, every tile, when K is chunked)
@@ -214,7 +257,7 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                 // dgz_aggregate_mean); the next row's count and positions load meanwhile
                 RowRef A[NR];
 #pragma unroll
-                for (int r = 0; r < NR; ++r) A[r] = row_ref(tile * kTileM + warp + r * kWarps, n, cnt, nbr, fanout, lane);
+                for (int r = 0; r < NR; ++r) A[r] = row_ref(r0 + warp + r * kWarps, lim, cnt, nbr, fanout, lane);
                 for (int rr = warp; rr < kTileM; rr += NR * kWarps) {
                     RowRef An[NR];
 #pragma unroll
@@ -222,7 +265,7 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                     if (rr + NR * kWarps < kTileM) {
 #pragma unroll
                         for (int r = 0; r < NR; ++r)
-                            An[r] = row_ref(tile * kTileM + rr + (NR + r) * kWarps, n, cnt, nbr, fanout, lane);
+                            An[r] = row_ref(r0 + rr + (NR + r) * kWarps, lim, cnt, nbr, fanout, lane);
                     }
                     for (int kb = 0; kb < Kc; kb += 128) {
                         const int kl = kb + lane * 4;
@@ -239,7 +282,7 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                 }
             } else {
                 for (int rr = warp; rr < kTileM; rr += kWarps) {   // scalar loads (dim % 4 != 0 or unaligned x)
-                    const RowRef A = row_ref(tile * kTileM + rr, n, cnt, nbr, fanout, lane);
+                    const RowRef A = row_ref(r0 + rr, lim, cnt, nbr, fanout, lane);
                     for (int kb = 0; kb < Kc; kb += 128) {
                         const int kl = kb + lane * 4, k0 = kc0 + kl;
                         float v[4] = {0.f, 0.f, 0.f, 0.f};
@@ -298,7 +341,7 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                 // store instruction writes 8 rows x 64 contiguous bytes instead of 32 rows x 16 B
                 const int quarter = warp & 3, group = warp >> 2;
                 uint8_t* stage = sA + warp * 2048;
-                const int64_t row0 = tile * kTileM + quarter * 32;
+                const int64_t row0 = r0 + quarter * 32;
                 for (int col = group * 16; col < N; col += 16 * (kWarps / 4)) {
                     uint32_t v[16];
                     const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col;
@@ -318,13 +361,13 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                     for (int it = 0; it < 4; ++it) {
                         const int idx = it * 32 + lane, r = idx >> 2, c = idx & 3;
                         const uint4 val = *reinterpret_cast<const uint4*>(stage + r * 64 + ((c ^ ((r >> 1) & 3)) * 16));
-                        if (row0 + r < n) *reinterpret_cast<uint4*>(y + (row0 + r) * (int64_t)N + col + c * 4) = val;
+                        if (row0 + r < lim) *reinterpret_cast<uint4*>(y + (row0 + r) * (int64_t)N + col + c * 4) = val;
                     }
                     __syncwarp();
                 }
             } else {
                 const int quarter = warp & 3, group = warp >> 2;   // direct: 8-column chunks
-                const int64_t row = tile * kTileM + quarter * 32 + lane;
+                const int64_t row = r0 + quarter * 32 + lane;
                 for (int col = group * 8; col < N; col += 8 * (kWarps / 4)) {
                     uint32_t v[8];
                     const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col;
@@ -333,7 +376,7 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                                    "=r"(v[7])
                                  : "r"(taddr));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (row < n) {
+                    if (row < lim) {
                         float4* dst = reinterpret_cast<float4*>(y + row * (int64_t)N + col);
                         dst[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
                                              __uint_as_float(v[3]));
@@ -361,17 +404,41 @@ using namespace dgz;
 // CTAs per SM (112 KiB), else the largest multiple of 128 that does (>= 128 for hidden <= 256); the
 // kernel then accumulates the chunks in TMEM, re-staging W's chunk for every tile.
 static int64_t sage_chunk(int64_t dim, int64_t hidden) {
-    const int64_t Kp = (dim + 15) / 16 * 16, budget = 112 * 1024 - 16;
+    const int64_t Kp = (dim + 15) / 16 * 16, budget = 112 * 1024 - 48;
     if ((hidden + kTileM) * Kp * 2 <= budget) return Kp;
     int64_t kc = budget / ((hidden + kTileM) * 2) / 128 * 128;
     return kc < 128 ? 128 : kc;
+}
+
+// Per-launch schedule slots for the dynamic tile schedule: a row counter and 256 per-SM arrival
+// counters, in a ring of kSchedSlots per device allocated once; each launch takes the next slot and
+// zeroes it on its own stream (as the gather's work counters).
+static constexpr int kSchedSlots = 1024, kSchedWords = 1 + 256;
+static unsigned long long* sched_slot(int dev) {
+    static std::mutex mu;
+    static unsigned long long* ring[64] = {};
+    static std::atomic<uint32_t> next[64];
+    if (dev < 0 || dev >= 64) return nullptr;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (!ring[dev]) {
+            unsigned long long* p = nullptr;
+            cudaStreamCaptureMode m = cudaStreamCaptureModeRelaxed;
+            cudaThreadExchangeStreamCaptureMode(&m);
+            const cudaError_t e = cudaMalloc((void**)&p, sizeof(unsigned long long) * kSchedSlots * kSchedWords);
+            cudaThreadExchangeStreamCaptureMode(&m);
+            if (e != cudaSuccess) return nullptr;
+            ring[dev] = p;
+        }
+    }
+    return ring[dev] + (size_t)(next[dev].fetch_add(1, std::memory_order_relaxed) % kSchedSlots) * kSchedWords;
 }
 
 extern "C" dgz_status dgz_sage_workspace(int64_t dim, int64_t hidden, int64_t* smem_bytes, int32_t* tmem_cols) {
     DGZ_REQUIRE(dim >= 1 && hidden >= 1, "dgz_sage_workspace: dim and hidden must be >= 1");
     uint32_t cols = 32;
     while (cols < (uint32_t)hidden && cols < 512) cols <<= 1;
-    if (smem_bytes) *smem_bytes = (hidden + kTileM) * sage_chunk(dim, hidden) * 2 + 16;
+    if (smem_bytes) *smem_bytes = (hidden + kTileM) * sage_chunk(dim, hidden) * 2 + 48;
     if (tmem_cols) *tmem_cols = (int32_t)cols;
     return DGZ_OK;
 }
@@ -410,17 +477,28 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
     const bool x_vec = (dim % 4 == 0) && (((uintptr_t)x & 15) == 0);   // float4 row loads
     const bool w_vec = (dim % 8 == 0) && (((uintptr_t)w_bf16 & 15) == 0);   // 16 B W loads
     const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(w_bf16);
+    int dev = 0;
+    DGZ_CUDA(cudaGetDevice(&dev));
+    // the dynamic schedule needs one pass over the rows per launch (repeat 1); DGZ_SAGE_STATIC=1 turns it off
+    static const bool force_static = getenv("DGZ_SAGE_STATIC") != nullptr;
+    auto sched_for = [&](int reps) -> unsigned long long* {
+        if (force_static || reps != 1) return nullptr;
+        unsigned long long* p = sched_slot(dev);
+        if (p && cudaMemsetAsync(p, 0, sizeof(unsigned long long) * kSchedWords, s) != cudaSuccess) return nullptr;
+        return p;
+    };
     if (ctas_per_sm > 0) {
         const int64_t c = (int64_t)k * ctas_per_sm;
         if (blocks > c) blocks = c;
         kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kc, (int)nchunk, nbr_local, cnt, fanout, n_dst_dev,
-                                                                     n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec, w_vec);
+                                                 n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec, w_vec,
+                                                 sched_for(repeat));
         dgz::count_launch();
     } else {
         for (int r = 0; r < repeat; ++r) {
             kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kc, (int)nchunk, nbr_local, cnt, fanout,
-                                                                         n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols,
-                                                                         y, 1, x_vec, w_vec);
+                                                     n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols, y, 1, x_vec, w_vec,
+                                                     sched_for(1));
             dgz::count_launch();
         }
     }

@@ -165,9 +165,9 @@ def test_sage_layer_edges(dev):
     dgz.sage_mean_linear(big.view(-1), 320, loc.view(-1), cnt, f, None, 10, wb, yb)
     torch.cuda.synchronize()
     check_layer(yb.cpu().numpy(), big.cpu().numpy(), loc[:10].cpu().numpy(), cnt[:10].cpu().numpy(), wb)
-    assert dgz.sage_workspace(128, 256) == ((256 + 128) * 128 * 2 + 16, 256)
-    assert dgz.sage_workspace(602, 256) == ((256 + 128) * 128 * 2 + 16, 256)     # K chunk 128
-    assert dgz.sage_workspace(200, 64) == ((64 + 128) * 208 * 2 + 16, 64)        # one chunk
+    assert dgz.sage_workspace(128, 256) == ((256 + 128) * 128 * 2 + 48, 256)
+    assert dgz.sage_workspace(602, 256) == ((256 + 128) * 128 * 2 + 48, 256)     # K chunk 128
+    assert dgz.sage_workspace(200, 64) == ((64 + 128) * 208 * 2 + 48, 64)        # one chunk
 
 
 def test_sage_layer_full_size_config4(dev):
