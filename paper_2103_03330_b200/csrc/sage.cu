@@ -18,11 +18,13 @@
 // is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns and a 56-register budget
 // are sized for it: 32 warps per SM keep the random row reads in flight, and a one-warp gather CTA
 // still fits beside them), so one CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
-// block (tools/consumer_roofline.py): 4.11 TB/s of algorithmic bytes (0.63 of HBM) with the dynamic
-// tile schedule (3.75 TB/s with one tile per CTA); the mean alone (dgz_aggregate_mean) 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
+// block (tools/consumer_roofline.py): 4.32 TB/s of algorithmic bytes (0.66 of HBM) with the dynamic
+// tile schedule and TMA tensor stores of y (3.75 TB/s with one tile per CTA and the warps' own stores);
+// the mean alone (dgz_aggregate_mean) 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
 // chunks through the free A buffer so stores are 64 B row segments.
 #include "internal.h"
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdlib.h>
 
@@ -150,7 +152,8 @@ __global__ void __maxnreg__(56)
 sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk, const int32_t* __restrict__ nbr,
                         const int32_t* __restrict__ cnt, int fanout, const int64_t* __restrict__ n_dst_dev, int64_t n_dst_max,
                         const __nv_bfloat16* __restrict__ w, int N, uint32_t tmem_cols, float* __restrict__ y, int repeat,
-                        bool x_vec, bool w_vec, unsigned long long* __restrict__ sched) {
+                        bool x_vec, bool w_vec, unsigned long long* __restrict__ sched,
+                        const __grid_constant__ CUtensorMap tmap_y, bool tma_y) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sB = smem;                                   // [N x Kc] bf16, core-matrix K-major (one K chunk of W)
     uint8_t* sA = smem + (size_t)N * Kc * 2;              // [128 x Kc] bf16 (the same K chunk of the means)
@@ -351,11 +354,28 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
                         : "r"(taddr));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    const int sw = (lane >> 1) & 3;   // 16 B-chunk swizzle: conflict-free both ways
+                    const bool tma = tma_y && row0 + 32 <= lim;   // the warp's 32 rows all live: one TMA store
+                    if (tma && lane == 0)   // the previous chunk's TMA store has read the staging buffer
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                    const int sw = (lane >> 1) & 3;   // 16 B-chunk swizzle (= the TMA's 64 B swizzle): conflict-free
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
                         *reinterpret_cast<uint4*>(stage + lane * 64 + ((c ^ sw) * 16)) =
                             make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                    if (tma) {
+                        // [32 rows x 16 fp32] box of y written by the TMA engine from the staging buffer
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmap_y),
+                                "r"(col), "r"((int32_t)row0), "r"(smem_u32(stage))
+                                : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                        continue;
+                    }
                     __syncwarp();
 #pragma unroll
                     for (int it = 0; it < 4; ++it) {
@@ -365,6 +385,9 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
                     }
                     __syncwarp();
                 }
+                if (tma_y && lane == 0)   // staging (= A) is rewritten by the next tile
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
             } else {
                 const int quarter = warp & 3, group = warp >> 2;   // direct: 8-column chunks
                 const int64_t row = r0 + quarter * 32 + lane;
@@ -390,6 +413,7 @@ sage_mean_linear_kernel(const float* __restrict__ x, int dim, int Kc, int nchunk
             __syncthreads();
         }
     }
+    if (tma_y && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // y written
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
@@ -432,6 +456,27 @@ static unsigned long long* sched_slot(int dev) {
         }
     }
     return ring[dev] + (size_t)(next[dev].fetch_add(1, std::memory_order_relaxed) % kSchedSlots) * kSchedWords;
+}
+
+// y as a TMA tensor ([rows][hidden] fp32, box 32 rows x 16 columns, 64 B swizzle = the staging layout)
+static bool make_y_map(CUtensorMap* m, float* y, int64_t rows, int64_t hidden) {
+    using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Enc enc = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (Enc) nullptr;
+        return reinterpret_cast<Enc>(p);
+    }();
+    if (!enc || rows <= 0 || rows > (int64_t(1) << 31)) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)hidden, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)hidden * 4};
+    const cuuint32_t box[2] = {16, 32}, estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 extern "C" dgz_status dgz_sage_workspace(int64_t dim, int64_t hidden, int64_t* smem_bytes, int32_t* tmem_cols) {
@@ -487,18 +532,23 @@ extern "C" dgz_status dgz_sage_mean_linear(const float* x, int64_t dim, const in
         if (p && cudaMemsetAsync(p, 0, sizeof(unsigned long long) * kSchedWords, s) != cudaSuccess) return nullptr;
         return p;
     };
+    // TMA stores of y for the staged epilogue (K chunk >= 128); DGZ_SAGE_NO_TMA=1 keeps the warps' stores
+    static const bool no_tma = getenv("DGZ_SAGE_NO_TMA") != nullptr;
+    CUtensorMap ymap;
+    memset(&ymap, 0, sizeof(ymap));
+    const bool tma_y = !no_tma && Kc >= 128 && make_y_map(&ymap, y, n_dst_max, hidden);
     if (ctas_per_sm > 0) {
         const int64_t c = (int64_t)k * ctas_per_sm;
         if (blocks > c) blocks = c;
         kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kc, (int)nchunk, nbr_local, cnt, fanout, n_dst_dev,
                                                  n_dst_max, w, (int)hidden, (uint32_t)cols, y, repeat, x_vec, w_vec,
-                                                 sched_for(repeat));
+                                                 sched_for(repeat), ymap, tma_y);
         dgz::count_launch();
     } else {
         for (int r = 0; r < repeat; ++r) {
             kern<<<(int)blocks, kThreads, smem, s>>>(x, (int)dim, (int)Kc, (int)nchunk, nbr_local, cnt, fanout,
                                                      n_dst_dev, n_dst_max, w, (int)hidden, (uint32_t)cols, y, 1, x_vec, w_vec,
-                                                     sched_for(1));
+                                                     sched_for(1), ymap, tma_y);
             dgz::count_launch();
         }
     }
