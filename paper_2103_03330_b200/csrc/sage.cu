@@ -12,16 +12,16 @@
 //   2. one thread issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = hidden, K = 16 per
 //      instruction, fp32 accumulate) with A and W from shared memory and D in tensor memory, and
 //      commits to an mbarrier;
-//   3. the sixteen warps read D back with tcgen05.ld (warp w: TMEM lanes 32(w%4).., 8-column chunks w/4 + 4c)
-//      and store y rows to HBM.
-// W is staged once per CTA in the same core-matrix layout (B operand, K-major).  The K dimension
-// is zero-padded to a multiple of 16.  Two CTAs share an SM (TMEM columns and a 56-register budget
-// are sized for it: 32 warps per SM keep the random row reads in flight, and a one-warp gather CTA
-// still fits beside them), so one CTA's MMA / epilogue overlaps the other's HBM-bound aggregation.  Measured on a config-4 last-hop
-// block (tools/consumer_roofline.py): 4.32 TB/s of algorithmic bytes (0.66 of HBM) with the dynamic
-// tile schedule and TMA tensor stores of y (3.75 TB/s with one tile per CTA and the warps' own stores);
-// the mean alone (dgz_aggregate_mean) 3.32 TB/s.  W arrives by cp.async while the first tile is summed; the epilogue stages 16-column
-// chunks through the free A buffer so stores are 64 B row segments.
+//   3. the sixteen warps read D back with tcgen05.ld (warp w: TMEM lanes 32(w%4).., 16-column chunks
+//      w/4 + 4c), stage each chunk in shared memory (64 B swizzle) and the TMA writes it to y.
+// W is staged once per resident CTA in the same core-matrix layout (B operand, K-major), by cp.async
+// while the first tile is summed; the K dimension is zero-padded to a multiple of 16 and chunked when
+// wider than the shared-memory budget.  Two CTAs share an SM (TMEM columns and a 56-register budget are
+// sized for it: 32 warps per SM keep the random row reads in flight, and a one-warp gather CTA still fits
+// beside them); tiles come from a per-launch row counter, the second CTA of an SM starting half a tile
+// behind.  Measured on a config-4 last-hop block (tools/consumer_roofline.py): 4.32 TB/s of algorithmic
+// bytes (0.66 of HBM; 3.75 TB/s with one tile per CTA and the warps' own stores); the mean alone
+// (dgz_aggregate_mean) 3.32 TB/s.
 #include "internal.h"
 
 #include <cuda.h>
