@@ -1,7 +1,8 @@
 """The a7 layer's measurements, checked on the committed B200 records (DESIGN.md sections 4 and 5.1):
 
 - the layer runs on the tensor cores: its SASS holds tcgen05 MMAs (UTCHMMA), the commit (UTCBAR), TMEM
-  loads (LDTM) and the TMEM allocator (UTCATOMSWS) (profiles/r02/sass_sage_tcgen05.txt);
+  loads (LDTM), the TMEM allocator (UTCATOMSWS) and TMA tensor stores of y (UTMASTG)
+  (profiles/r02/sass_sage_tcgen05.txt);
 - it is HBM-bound: on the config-4 last hop it moves >= 0.5 of the measured HBM bandwidth in
   algorithmic bytes, the GEMM is a few percent of its time (tensor pipe < 5 % active), and ncu's DRAM
   bytes stay below the algorithmic bytes (re-read neighbour rows hit L2)
@@ -25,7 +26,7 @@ def _jsonl(name):
 
 def test_layer_sass_is_tcgen05():
     txt = open(os.path.join(P, "sass_sage_tcgen05.txt")).read()
-    for op in ("UTCHMMA", "UTCBAR", "LDTM", "UTCATOMSWS", "LDGSTS"):
+    for op in ("UTCHMMA", "UTCBAR", "LDTM", "UTCATOMSWS", "LDGSTS", "UTMASTG"):
         assert op in txt, op
 
 
